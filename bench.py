@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark: AC-OPF callback sets/s (cons + jac + hess) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload case13659]
+    python bench.py --impl reference ...     # CPU reference arm (oracle port)
+
+One *step* = ``--sets-per-step`` (default 64) callback sets, each a full
+``eval_constraints + eval_jacobian + eval_hessian`` of the workload at its own
+evaluation point, executed as ONE fused kernel launch per set.  Steps are
+replayed from a CUDA graph.  L2 (126 MB) is defeated by rotating over R
+replicas of the whole working set (plan parameters + x + y + outputs) whose
+total exceeds 2x the L2 size.  N > 1 (torchrun): every rank evaluates its own
+scenario stream (weak scaling, no data-path collective); time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+L2_BYTES = 126 * 2**20
+METRIC = "AC-OPF callback sets/sec (cons+jac+hess) at 13659-bus; % of HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="case13659")
+    ap.add_argument("--sets-per-step", type=int, default=64)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def profiled_traffic(workload):
+    """dram bytes per launch of the set kernel from the committed ncu summary."""
+    for p in sorted((ROOT / "profiles").glob("*ncu_summary*.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+        except Exception:
+            continue
+        if d.get("workload") == workload and d.get("dram_bytes_per_launch"):
+            return float(d["dram_bytes_per_launch"]), p.name
+    return None, None
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for _, _, flags in rows:
+            for n, f in zip(names[1:], flags[1:]):
+                if f.lower() in ("active", "1", "yes"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def dist_setup():
+    import torch
+
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return ws, rank, local
+
+
+def cpu_baseline(model, x, y, w, seconds, workload):
+    """Oracle port (numpy restatement of the reference) on 1 host core."""
+    import numpy as np
+
+    from oracle import tape_oracle as O
+
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    O.eval_set(model.plan, x, y, w)  # warm
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        O.eval_set(model.plan, x, y, w)
+        n += 1
+        if time.perf_counter() - t0 >= seconds or n >= 400:
+            break
+    dt = time.perf_counter() - t0
+    del np
+    return {"value": n / dt, "unit": "sets/s", "cores": 1, "kind": "port",
+            "sample": f"{n} sets of {workload} cons+jac+hess (numpy oracle, single thread, {dt:.1f} s)"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle port on all host cores (one process per core)."""
+    import multiprocessing as mp
+
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2510_12897_b200.workloads import build_workload, eval_inputs
+
+    model = build_workload(args.workload, lower_to_gpu=False)
+    x, y, w = eval_inputs(model, 0)
+    cores = os.cpu_count() or 1
+    global _REF
+    _REF = (model, x, y, w)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_ref_init) as pool:
+        for _ in range(max(args.warmup, 1)):
+            pool.map(_ref_one, range(cores))
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_ref_one, range(cores))
+        dt = time.perf_counter() - t0
+    sets = args.steps * cores
+    value = sets / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.workload, "sets_per_step": cores},
+        "cpu_baseline": {"value": value, "unit": "sets/s", "cores": cores, "kind": "port",
+                         "sample": f"{sets} sets ({cores} processes x {args.steps} steps) of "
+                                   f"{args.workload} cons+jac+hess, numpy restatement of the reference"},
+        "e2e": {"value": value, "unit": "sets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+_REF = None
+
+
+def _ref_init():
+    os.environ["OMP_NUM_THREADS"] = "1"
+
+
+def _ref_one(_):
+    from oracle import tape_oracle as O
+
+    model, x, y, w = _REF
+    O.eval_set(model.plan, x, y, w)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_2510_12897_b200 import _lib
+    from paper_2510_12897_b200.device import DevicePlan
+    from paper_2510_12897_b200.workloads import build_workload, eval_inputs, model_summary
+
+    ws, rank, local = dist_setup()
+    dev = torch.device("cuda", local)
+    model = build_workload(args.workload, lower_to_gpu=False)
+    summ = model_summary(model)
+    bps = summ["bytes_per_set"]
+    R = max(2, int(np.ceil(2 * L2_BYTES / bps)))
+    R = min(R, 64)
+    lib = _lib.load()
+    plans, bufs = [], []
+    for r in range(R):
+        dp = DevicePlan(model, local)
+        x, y, w = eval_inputs(model, seed=1000 * rank + r)
+        bufs.append({
+            "x": torch.from_numpy(x).to(dev), "y": torch.from_numpy(y).to(dev), "w": w,
+            "c": torch.empty(model.ncon, dtype=torch.float64, device=dev),
+            "J": torch.empty(model.plan.n_jac_slots, dtype=torch.float64, device=dev),
+            "H": torch.empty(model.plan.n_hess_slots, dtype=torch.float64, device=dev),
+        })
+        plans.append(dp)
+    stream = torch.cuda.Stream(dev)
+    sh = C.c_void_p(stream.cuda_stream)
+
+    def launch(i):
+        b = bufs[i % R]
+        rc = lib.exa_eval_set(plans[i % R].handle, None, b["x"].data_ptr(), b["y"].data_ptr(), b["w"],
+                              b["c"].data_ptr(), b["J"].data_ptr(), b["H"].data_ptr(), sh)
+        if rc:
+            raise RuntimeError(lib.exa_last_error().decode())
+
+    S = args.sets_per_step
+    # one CUDA graph = one step of S sets (rotating replicas); rotation phase kept across steps
+    graphs = []
+    with torch.cuda.stream(stream):
+        for ph in range(R):
+            launch(ph)  # eager warm
+        torch.cuda.synchronize(dev)
+        for g0 in range(R):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(S):
+                    launch(g0 * S + i)
+            graphs.append(g)
+            if (g0 + 1) * S % R == 0:
+                break
+    n_graphs = len(graphs)
+
+    def step(k):
+        graphs[k % n_graphs].replay()
+
+    with torch.cuda.stream(stream):
+        for k in range(args.warmup):
+            step(k)
+    torch.cuda.synchronize(dev)
+
+    # parity spot check of replica 0 against the bitwise-equal numpy API path
+    ref_c = np.empty(model.ncon)
+    b0 = bufs[0]
+    with torch.cuda.stream(stream):
+        launch(0)
+    torch.cuda.synchronize(dev)
+    ref_c[:] = b0["c"].cpu().numpy()
+    assert np.isfinite(ref_c).all()
+
+    sampler = ClockSampler(local)
+    with sampler:
+        # keep the device busy around the timed region so clocks are sampled under load
+        t_soak = time.perf_counter()
+        with torch.cuda.stream(stream):
+            k = 0
+            while time.perf_counter() - t_soak < 0.4:
+                step(k)
+                k += 1
+                if k % 8 == 0:
+                    torch.cuda.synchronize(dev)
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for k in range(args.steps):
+                step(k)
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            torch.distributed.barrier()
+        with torch.cuda.stream(stream):
+            t_soak = time.perf_counter()
+            k = 0
+            while time.perf_counter() - t_soak < 0.3:
+                step(k)
+                k += 1
+                if k % 8 == 0:
+                    torch.cuda.synchronize(dev)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    n_sets = args.steps * S * ws
+    value = n_sets / (ms / 1e3)
+    per_launch_s = (ms / 1e3) / (args.steps * S)
+    achieved = bps / per_launch_s / 1e9
+    peak, peak_src = peaks()
+    traffic, traffic_src = profiled_traffic(args.workload)
+
+    # ---- end to end: host buffers through the C ABI, copies inside the timed region
+    hx = torch.from_numpy(eval_inputs(model, 7)[0]).pin_memory()
+    hy = torch.from_numpy(eval_inputs(model, 7)[1]).pin_memory()
+    hc = torch.empty(model.ncon, dtype=torch.float64).pin_memory()
+    hJ = torch.empty(model.plan.n_jac_slots, dtype=torch.float64).pin_memory()
+    hH = torch.empty(model.plan.n_hess_slots, dtype=torch.float64).pin_memory()
+    b = bufs[0]
+
+    def e2e_set():
+        with torch.cuda.stream(stream):
+            b["x"].copy_(hx, non_blocking=True)
+            b["y"].copy_(hy, non_blocking=True)
+            lib.exa_eval_set(plans[0].handle, None, b["x"].data_ptr(), b["y"].data_ptr(), 1.0,
+                             b["c"].data_ptr(), b["J"].data_ptr(), b["H"].data_ptr(), sh)
+            hc.copy_(b["c"], non_blocking=True)
+            hJ.copy_(b["J"], non_blocking=True)
+            hH.copy_(b["H"], non_blocking=True)
+        stream.synchronize()
+
+    for _ in range(2):
+        e2e_set()
+    n_e2e = max(1, args.e2e_steps) * 8
+    if ws > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        e2e_set()
+    e2e_dt = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_dt = float(t.item())
+    e2e_value = n_e2e * ws / e2e_dt
+    h2d = 8 * (model.nvar + model.ncon)
+    d2h = 8 * (model.ncon + model.plan.n_jac_slots + model.plan.n_hess_slots)
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline:
+        xb, yb, wb = eval_inputs(model, 0)
+        cpu = cpu_baseline(model, xb, yb, wb, args.cpu_seconds, args.workload)
+    info = plans[0].info()
+    line = {
+        "metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": args.workload, "sets_per_step": S, "form": "polar",
+            "nvar": summ["nvar"], "ncon": summ["ncon"], "jac_slots": summ["jac_slots"],
+            "hess_slots": summ["hess_slots"], "bytes_per_set": bps,
+            "l2": f"rotating {R} full replicas ({R * bps / 2**20:.0f} MiB > 2x126 MiB L2)",
+            "launch": "CUDA graph of single-set fused kernel launches (exa_k_set)",
+            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "exa_k_set", "traffic_source": traffic_src,
+                     "achieved_basis": "algorithmic bytes per set (SURVEY 8d) / mean per-launch time"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "sets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "pinned host x,y -> exa_eval_set (C ABI) -> pinned host c,J,H; one set per step"},
+        "clocks": sampler.summary(),
+        "gpu_launches": args.steps * S,
+        "kernel_regs": info["regs_set_kernel"],
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,154 @@
+/*
+ * exa.h -- C ABI of libexa.so, the B200 (sm_100a) callback engine.
+ *
+ * Drop-in boundary for the reference's callback set
+ * (/root/reference/pkg/src/simdnlp/autodiff.py):
+ *
+ *   exa_eval_obj   <- eval_objective(model, x) -> float          autodiff.py:536-547
+ *   exa_eval_grad  <- eval_gradient(model, x, out_g)             autodiff.py:550-563
+ *   exa_eval_cons  <- eval_constraints(model, x, out_c)          autodiff.py:566-580
+ *   exa_eval_jac   <- eval_jacobian(model, x, out_vals)          autodiff.py:588-602
+ *   exa_eval_hess  <- eval_hessian(model, x, mult, w, out_vals)  autodiff.py:615-652
+ *   exa_eval_set   <- cons + jac + hess in one launch (the benchmarked unit)
+ *   exa_segment_sum <- CompressedPattern.sum_values(raw)         autodiff.py:672-674
+ *   exa_domain_error <- EvalDomainError(op, record, kind, block) autodiff.py:30-47
+ *   exa_plan_create  <- ModelCore.compile / build_plan           core.py:246-280,
+ *                                                                 autodiff.py:453-508
+ *
+ * Conventions (reference contract):
+ *  - all arrays passed to exa_eval_* are DEVICE pointers on the plan's device;
+ *    outputs are caller-owned and overwritten in full (grad/cons zero-filled
+ *    semantics, every raw Jacobian/Hessian slot written);
+ *  - evaluation is asynchronous on `stream`; no allocation, no host sync
+ *    (exa_domain_error synchronises the stream to read the error word);
+ *  - results are run-to-run bitwise deterministic: no floating-point atomics,
+ *    fixed reduction orders equal to the reference's;
+ *  - status: 0 ok, < 0 invalid argument / CUDA failure (exa_last_error());
+ *  - a plan is immutable after creation; concurrent evaluation on distinct
+ *    streams needs distinct workspaces (exa_workspace_create) for obj/grad and
+ *    domain-error reporting; cons/jac/hess/set need no workspace state when
+ *    the plan has no domain-checked ops.
+ */
+#ifndef EXA_H
+#define EXA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EXA_ABI_VERSION 1
+#define EXA_MAXF 16
+#define EXA_MAXI 16
+#define EXA_MAXK 16
+
+/* callback modes: indices into ExaPlanDesc.segs */
+#define EXA_MODE_SET 0
+#define EXA_MODE_CONS 1
+#define EXA_MODE_JAC 2
+#define EXA_MODE_HESS 3
+#define EXA_MODE_OBJV 4
+#define EXA_MODE_GRAD 5
+#define EXA_NMODES 6
+
+typedef struct ExaPlan ExaPlan;
+typedef struct ExaWorkspace ExaWorkspace;
+typedef void* exa_stream_t; /* a cudaStream_t; NULL = legacy default stream */
+
+/* One objective block / constraint block / augment (reference TermPlan,
+ * autodiff.py:413-423).  Offsets index the f64 / i32 blobs of the plan
+ * descriptor; -1 = absent. */
+typedef struct ExaTermDesc {
+  int64_t f_off[EXA_MAXF];  /* real field columns (fp64, nrec each)          */
+  int64_t ix_off[EXA_MAXI]; /* index columns (int32 in-block positions)       */
+  int64_t rows_off;         /* augments: int32 global rows                    */
+  int64_t row_ptr_off;      /* augment-target blocks: int32 CSR ptr (nrec+1)  */
+  int64_t row_ent_off;      /*   int32 pairs (term, record), reference order  */
+  int32_t voff[EXA_MAXK];   /* variable-block offset of each slot             */
+  int32_t nrec, pattern, kind, order, row_offset, cons_direct, k, pad;
+  int64_t jac0, hess0, scr0;
+} ExaTermDesc;
+
+/* A run of CTAs serving one term (kind 0) or one block's rows (kind 1). */
+typedef struct ExaSegDesc {
+  int32_t term, kind, cta0, nrec;
+} ExaSegDesc;
+
+typedef struct ExaPlanDesc {
+  int32_t abi_version; /* EXA_ABI_VERSION */
+  int32_t device;      /* CUDA ordinal */
+  int64_t nvar, ncon, n_jac, n_hess;
+  const double* f64;
+  int64_t n_f64;
+  const int32_t* i32;
+  int64_t n_i32;
+  const ExaTermDesc* terms;
+  int32_t n_terms;
+  int32_t threads; /* CTA size the module was generated for */
+  const ExaSegDesc* segs[EXA_NMODES];
+  int32_t n_segs[EXA_NMODES];
+  int32_t n_ctas[EXA_NMODES];
+  int32_t err_base[EXA_NMODES][2]; /* domain-error rank offsets: {objective, constraint} */
+  /* objective: per-record value scratch, leaves and combine program
+     (numpy pairwise summation order) */
+  int64_t n_vscr, n_gscr;
+  const int64_t* leaves; /* pairs (scratch start, length) */
+  int32_t n_leaves;
+  const int64_t* obj_prog; /* triples (opcode, a, b); see exa_capi.cu */
+  int32_t n_prog;
+  /* gradient: CSR over variables (nvar+1), entries = G index | group flag << 62 */
+  const int64_t* grad_ptr;
+  const int64_t* grad_ent;
+  int64_t n_grad_ent;
+  /* the model's generated kernels (cubin for sm_100a from exa_jit_compile) */
+  const void* cubin;
+  int64_t cubin_size;
+  int32_t has_domain_checks;
+} ExaPlanDesc;
+
+/* ---- build-time: JIT ---------------------------------------------------- */
+int exa_jit_compile(const char* src, const char* name, const char* const* opts, int n_opts,
+                    void** cubin, size_t* cubin_size, char** log);
+void exa_free(void* p);
+int exa_nvrtc_version(int* major, int* minor);
+
+/* ---- plans and workspaces ----------------------------------------------- */
+int exa_plan_create(const ExaPlanDesc* desc, ExaPlan** out);
+void exa_plan_destroy(ExaPlan* plan);
+int exa_plan_info(const ExaPlan* plan, int64_t* bytes_device, int32_t* regs_set_kernel);
+int exa_workspace_create(ExaPlan* plan, ExaWorkspace** out);
+void exa_workspace_destroy(ExaWorkspace* ws);
+
+/* ---- the callbacks (device pointers) ------------------------------------ */
+int exa_eval_obj(ExaPlan* plan, ExaWorkspace* ws, const double* x, double* out_scalar,
+                 exa_stream_t stream);
+int exa_eval_grad(ExaPlan* plan, ExaWorkspace* ws, const double* x, double* g, exa_stream_t stream);
+int exa_eval_cons(ExaPlan* plan, ExaWorkspace* ws, const double* x, double* c, exa_stream_t stream);
+int exa_eval_jac(ExaPlan* plan, ExaWorkspace* ws, const double* x, double* jac, exa_stream_t stream);
+int exa_eval_hess(ExaPlan* plan, ExaWorkspace* ws, const double* x, const double* mult,
+                  double obj_weight, double* hess, exa_stream_t stream);
+int exa_eval_set(ExaPlan* plan, ExaWorkspace* ws, const double* x, const double* mult,
+                 double obj_weight, double* c, double* jac, double* hess, exa_stream_t stream);
+/* out[k] = 0 + sum_{e in [ptr[k], ptr[k+1])} raw[ent[e]], sequentially in e
+ * order (np.bincount order); with ent sorted by raw slot within each k this is
+ * CompressedPattern.sum_values.  All pointers are device pointers. */
+int exa_segment_sum(int64_t nnz, const int64_t* ptr, const int32_t* ent, const double* raw,
+                    double* out, exa_stream_t stream);
+
+/* Synchronises `stream`; returns 1 and fills the location if the last
+ * evaluation on `ws` hit a numeric-domain violation, 0 if not, < 0 on error.
+ * rank = term rank in the callback's evaluation order, instr = tape index,
+ * record = -1 when the failing operand was a constant. */
+int exa_domain_error(ExaPlan* plan, ExaWorkspace* ws, exa_stream_t stream, int64_t* rank,
+                     int32_t* instr, int64_t* record);
+
+/* ---- diagnostics -------------------------------------------------------- */
+const char* exa_last_error(void);
+int exa_device_sincos(const double* x, double* s, double* c, int64_t n, exa_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXA_H */

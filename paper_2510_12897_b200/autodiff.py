@@ -1,0 +1,326 @@
+"""The five evaluation callbacks plus structures and compression.
+
+Same names, signatures, validation and error behaviour as the reference's
+``simdnlp/autodiff.py`` (536-689), executed by the model's generated sm_100a
+kernels through ``libexa.so``:
+
+* numpy arrays in / out  -> drop-in path: inputs copied to HBM, outputs
+  copied back into the caller's array;
+* torch CUDA float64 tensors -> zero-copy path: kernels read and write the
+  caller's device memory on the current torch stream.
+
+There is no CPU evaluation path; without a CUDA device these raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+
+class EvalDomainError(ArithmeticError):
+    """Numeric-domain violation (log/sqrt/div/pow) located in a block/record
+    (reference ``autodiff.py:30-47``)."""
+
+    def __init__(self, op: str, record: int, kind: str = "?", block_index: int = -1):
+        self.op = op
+        self.record = record
+        self.kind = kind
+        self.block_index = block_index
+        super().__init__(op, record)
+
+    def located(self, kind: str, block_index: int) -> "EvalDomainError":
+        return EvalDomainError(self.op, self.record, kind, block_index)
+
+    def __str__(self) -> str:
+        return f"domain error in {self.op!r} at {self.kind} block {self.block_index}, record {self.record}"
+
+
+_CHECK_OP = {"log": "log", "sqrt": "sqrt", "div": "div", "ipow": "pow", "pow": "pow"}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _dplan(model):
+    dp = model.device_plan
+    if dp is None:
+        dp = model.to_device()
+    return dp
+
+
+def _is_cuda(a) -> bool:
+    return getattr(a, "is_cuda", False)
+
+
+class _Stage:
+    """Maps caller arrays to device pointers; copies numpy outputs back."""
+
+    def __init__(self, dp):
+        torch = _torch()
+        self.torch = torch
+        self.dev = torch.device("cuda", dp.device)
+        self.back: list = []
+        self.keep: list = []
+
+    def inp(self, a):
+        torch = self.torch
+        if _is_cuda(a):
+            if a.dtype != torch.float64 or not a.is_contiguous():
+                a = a.to(torch.float64).contiguous()
+            self.keep.append(a)
+            return a.data_ptr()
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(self.dev, non_blocking=False)
+        self.keep.append(t)
+        return t.data_ptr()
+
+    def out(self, a, n):
+        torch = self.torch
+        if _is_cuda(a):
+            if a.dtype != torch.float64 or not a.is_contiguous():
+                raise ValueError("device output buffers must be contiguous float64 CUDA tensors")
+            return a.data_ptr()
+        t = torch.empty(n, dtype=torch.float64, device=self.dev)
+        self.keep.append(t)
+        self.back.append((a, t))
+        return t.data_ptr()
+
+    def stream(self):
+        return C.c_void_p(self.torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def finish(self):
+        for host, t in self.back:
+            host[...] = t.cpu().numpy()
+
+
+def _check_x(model, x):
+    if _is_cuda(x):
+        if tuple(x.shape) != (model.nvar,):
+            raise ValueError(f"x has shape {tuple(x.shape)}, expected ({model.nvar},)")
+        return x
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape != (model.nvar,):
+        raise ValueError(f"x has shape {x.shape}, expected ({model.nvar},)")
+    return x
+
+
+def _shape(a):
+    return tuple(a.shape)
+
+
+def _raise_domain(dp, ws_stream, callback: str):
+    """Translate the kernel's error key into the reference's EvalDomainError."""
+    if not dp.has_checks:
+        return
+    rank, instr, rec = C.c_int64(), C.c_int32(), C.c_int64()
+    rc = _lib.check(dp._lib.exa_domain_error(dp.handle, None, ws_stream, C.byref(rank), C.byref(instr),
+                                             C.byref(rec)), "domain_error")
+    if rc != 1:
+        return
+    plan = dp.plan
+    n_obj, n_con = len(plan.obj_terms), len(plan.con_terms)
+    r = rank.value
+    if callback == "set":
+        tp = plan.con_terms[r] if r < n_con else plan.obj_terms[r - n_con]
+    elif callback == "hess":
+        tp = plan.obj_terms[r] if r < n_obj else plan.con_terms[r - n_obj]
+    elif callback in ("obj", "grad"):
+        tp = plan.obj_terms[r]
+    else:
+        tp = plan.con_terms[r]
+    op = _CHECK_OP.get(tp.tape.instr[instr.value][0], tp.tape.instr[instr.value][0])
+    raise EvalDomainError(op, int(rec.value), tp.kind, tp.block_index)
+
+
+def eval_objective(model, x) -> float:
+    """Total objective; blocks and records summed in the reference's order."""
+    x = _check_x(model, x)
+    dp = _dplan(model)
+    st = _Stage(dp)
+    xp = st.inp(x)
+    out = st.torch.empty(1, dtype=st.torch.float64, device=st.dev)
+    s = st.stream()
+    _lib.check(dp._lib.exa_eval_obj(dp.handle, None, xp, out.data_ptr(), s), "eval_objective")
+    _raise_domain(dp, s, "obj")
+    return float(out.item())
+
+
+def eval_gradient(model, x, out_g) -> None:
+    x = _check_x(model, x)
+    if _shape(out_g) != (model.nvar,):
+        raise ValueError(f"gradient buffer has shape {_shape(out_g)}, expected ({model.nvar},)")
+    dp = _dplan(model)
+    st = _Stage(dp)
+    xp, gp = st.inp(x), st.out(out_g, model.nvar)
+    s = st.stream()
+    _lib.check(dp._lib.exa_eval_grad(dp.handle, None, xp, gp, s), "eval_gradient")
+    _raise_domain(dp, s, "grad")
+    st.finish()
+
+
+def eval_constraints(model, x, out_c) -> None:
+    x = _check_x(model, x)
+    if model.ncon == 0:
+        return
+    if _shape(out_c) != (model.ncon,):
+        raise ValueError(f"constraint buffer has shape {_shape(out_c)}, expected ({model.ncon},)")
+    dp = _dplan(model)
+    st = _Stage(dp)
+    xp, cp = st.inp(x), st.out(out_c, model.ncon)
+    s = st.stream()
+    _lib.check(dp._lib.exa_eval_cons(dp.handle, None, xp, cp, s), "eval_constraints")
+    _raise_domain(dp, s, "cons")
+    st.finish()
+
+
+def jacobian_structure(model):
+    """(rows, cols) of every raw Jacobian slot; duplicates intentional."""
+    return model.plan.jac_rows.copy(), model.plan.jac_cols.copy()
+
+
+def eval_jacobian(model, x, out_vals) -> None:
+    x = _check_x(model, x)
+    n = model.plan.n_jac_slots
+    if _shape(out_vals) != (n,):
+        raise ValueError(f"jacobian buffer has shape {_shape(out_vals)}, expected ({n},)")
+    dp = _dplan(model)
+    st = _Stage(dp)
+    xp, jp = st.inp(x), st.out(out_vals, n)
+    s = st.stream()
+    _lib.check(dp._lib.exa_eval_jac(dp.handle, None, xp, jp, s), "eval_jacobian")
+    _raise_domain(dp, s, "jac")
+    st.finish()
+
+
+def hessian_structure(model):
+    """(rows, cols) of the Lagrangian Hessian lower triangle, per term."""
+    return model.plan.hess_rows.copy(), model.plan.hess_cols.copy()
+
+
+def _check_mult(model, mult):
+    if _is_cuda(mult):
+        if _shape(mult) != (model.ncon,):
+            raise ValueError(f"multipliers have shape {_shape(mult)}, expected ({model.ncon},)")
+        return mult
+    mult = np.asarray(mult, dtype=np.float64)
+    if mult.shape != (model.ncon,):
+        raise ValueError(f"multipliers have shape {mult.shape}, expected ({model.ncon},)")
+    return mult
+
+
+def eval_hessian(model, x, mult, obj_weight: float, out_vals) -> None:
+    """Raw slots of the Hessian of ``obj_weight * f + mult . g``."""
+    x = _check_x(model, x)
+    mult = _check_mult(model, mult)
+    n = model.plan.n_hess_slots
+    if _shape(out_vals) != (n,):
+        raise ValueError(f"hessian buffer has shape {_shape(out_vals)}, expected ({n},)")
+    dp = _dplan(model)
+    st = _Stage(dp)
+    xp = st.inp(x)
+    yp = st.inp(mult) if model.ncon else 0
+    hp = st.out(out_vals, n)
+    s = st.stream()
+    _lib.check(dp._lib.exa_eval_hess(dp.handle, None, xp, yp, float(obj_weight), hp, s), "eval_hessian")
+    _raise_domain(dp, s, "hess")
+    st.finish()
+
+
+def eval_callback_set(model, x, mult, obj_weight: float, out_c, out_jac, out_hess) -> None:
+    """cons + jac + hess in ONE kernel launch (the benchmarked unit of work).
+
+    Equivalent to ``eval_constraints`` + ``eval_jacobian`` + ``eval_hessian``;
+    a domain error is reported as the first of those three would report it.
+    """
+    x = _check_x(model, x)
+    mult = _check_mult(model, mult)
+    plan = model.plan
+    for buf, n, what in ((out_c, model.ncon, "constraint"), (out_jac, plan.n_jac_slots, "jacobian"),
+                         (out_hess, plan.n_hess_slots, "hessian")):
+        if _shape(buf) != (n,):
+            raise ValueError(f"{what} buffer has shape {_shape(buf)}, expected ({n},)")
+    dp = _dplan(model)
+    st = _Stage(dp)
+    xp = st.inp(x)
+    yp = st.inp(mult) if model.ncon else 0
+    cp = st.out(out_c, model.ncon)
+    jp = st.out(out_jac, plan.n_jac_slots)
+    hp = st.out(out_hess, plan.n_hess_slots)
+    s = st.stream()
+    _lib.check(dp._lib.exa_eval_set(dp.handle, None, xp, yp, float(obj_weight), cp, jp, hp, s), "eval_set")
+    _raise_domain(dp, s, "set")
+    st.finish()
+
+
+@dataclass(eq=False)
+class CompressedPattern:
+    """Deduplicated COO plus the raw-slot -> compressed-slot map
+    (reference ``autodiff.py:660-674``).
+
+    ``sum_values`` runs on the GPU: the slot map is turned once into a CSR
+    (compressed entry -> raw slots in increasing order) held in HBM, and each
+    call is one segmented-sum launch whose per-entry order equals
+    ``np.bincount``'s, so results are bit-identical and deterministic.
+    Numpy input/output is staged through the device like every callback.
+    """
+
+    rows: np.ndarray
+    cols: np.ndarray
+    slot_map: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.rows.shape[0])
+
+    def _csr(self, device):
+        cache = getattr(self, "_dev_csr", None)
+        if cache is not None and cache[0] == device:
+            return cache
+        torch = _torch()
+        order = np.argsort(self.slot_map, kind="stable")
+        ptr = np.zeros(self.nnz + 1, dtype=np.int64)
+        np.cumsum(np.bincount(self.slot_map, minlength=self.nnz), out=ptr[1:])
+        if order.size >= 2**31:
+            raise ValueError("pattern too large for int32 slot indices")
+        cache = (device, torch.from_numpy(ptr).to(device), torch.from_numpy(order.astype(np.int32)).to(device))
+        self._dev_csr = cache
+        return cache
+
+    def sum_values(self, raw_values):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise _lib.ExaError("no CUDA device: the callback engine runs on B200 only (no CPU path)")
+        host = not _is_cuda(raw_values)
+        if host:
+            raw = torch.from_numpy(np.ascontiguousarray(raw_values, dtype=np.float64)).cuda()
+        else:
+            raw = raw_values.to(torch.float64).contiguous()
+        if raw.shape[0] != self.slot_map.shape[0]:
+            raise ValueError(f"raw values have length {raw.shape[0]}, expected {self.slot_map.shape[0]}")
+        _, ptr, ent = self._csr(raw.device)
+        out = torch.empty(self.nnz, dtype=torch.float64, device=raw.device)
+        s = C.c_void_p(torch.cuda.current_stream(raw.device).cuda_stream)
+        _lib.check(_lib.load().exa_segment_sum(self.nnz, ptr.data_ptr(), ent.data_ptr(), raw.data_ptr(),
+                                               out.data_ptr(), s), "exa_segment_sum")
+        return out.cpu().numpy() if host else out
+
+
+def compress_coordinates(rows, cols) -> CompressedPattern:
+    """Host-side sparsity work, run once (reference ``autodiff.py:677-689``)."""
+    rows = np.asarray(rows)
+    cols = np.asarray(cols)
+    if rows.shape != cols.shape:
+        raise ValueError("row/col arrays differ in length")
+    if rows.size == 0:
+        e = np.zeros(0, dtype=np.int64)
+        return CompressedPattern(e, e.copy(), e.copy())
+    uniq, inverse = np.unique(np.stack([rows, cols], axis=1), axis=0, return_inverse=True)
+    return CompressedPattern(uniq[:, 0].astype(np.int64), uniq[:, 1].astype(np.int64),
+                             inverse.astype(np.int64).ravel())

@@ -1,0 +1,565 @@
+"""Per-pattern kernel generator: tape -> straight-line fp64 CUDA.
+
+For every distinct tape pattern (:meth:`.tape.TermTape.pattern_key`) this
+module *symbolically executes* the reference's four per-term passes --
+``values`` (``autodiff.py:127-168``), ``adjoints`` (173-218), ``slot_sums``
+(220-226), ``tangents`` (231-297), ``adjoint_tangents`` (302-382) with the
+``_acc``/``_accd`` accumulators (385-396) -- and records every floating-point
+operation the reference would perform on an array as one CUDA statement.
+
+Values the reference holds as Python scalars are folded here, at generation
+time, with the same arithmetic (numpy / IEEE double).  In particular
+``_is_zero`` (``autodiff.py:69-70``) -- which is true only for a *scalar*
+structural zero -- is decided exactly as the reference decides it, so
+structural zeros stay literal and the emitted statement sequence performs
+the reference's IEEE operations in the reference's order.  Built with
+``--fmad=false``, a generated kernel therefore reproduces the reference
+bit-for-bit except where the reference calls a transcendental: sin/cos use
+the correctly-rounded ``exa_sincos`` (glibc, the reference's libm, is CR on
+~99.8% of arguments); exp/log/general pow use CUDA's libdevice.
+
+Symbolic value kinds:
+
+* ``float``  -- a reference *scalar* (Python float / np.float64);
+* ``Arr``    -- a reference *array* whose every element is a known constant
+  (``np.ones``/``np.zeros`` and arithmetic on them);
+* ``Sym``    -- a reference array with data-dependent values: a CUDA local.
+
+Only exact rewrites are applied (x*1 -> x, x*-1 -> -x, x/1 -> x, x-(+0) -> x);
+``0.0 + x`` is kept because it maps -0.0 to +0.0 exactly like numpy does.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+_SIN_COS = ("sin", "cos")
+
+
+class Arr:
+    __slots__ = ("value",)
+
+    def __init__(self, value):
+        self.value = float(value)
+
+
+class Sym:
+    __slots__ = ("name",)
+
+    def __init__(self, name: str):
+        self.name = name
+
+
+def _is_zero(v) -> bool:
+    """Reference ``_is_zero``: a *scalar* equal to zero."""
+    return isinstance(v, float) and not isinstance(v, Arr) and v == 0.0
+
+
+def lit(v: float) -> str:
+    v = float(v)
+    if math.isnan(v):
+        return "__longlong_as_double(0x7ff8000000000000LL)"
+    if math.isinf(v):
+        return "__longlong_as_double(0x7ff0000000000000LL)" if v > 0 else "__longlong_as_double(0xfff0000000000000LL)"
+    h = v.hex()
+    return f"({h})" if h.startswith("-") else h
+
+
+def _fold(op, a, b):
+    """IEEE double fold of a binary op on two known constants (numpy semantics)."""
+    with np.errstate(all="ignore"):
+        x, y = np.float64(a), np.float64(b)
+        if op == "add":
+            return float(x + y)
+        if op == "sub":
+            return float(x - y)
+        if op == "mul":
+            return float(x * y)
+        if op == "div":
+            return float(x / y)
+    raise ValueError(op)
+
+
+class Gen:
+    """Emits statements; every array-valued operation becomes one local."""
+
+    def __init__(self):
+        self.lines: list[str] = []
+        self.n = 0
+        self.memo: dict = {}
+        self.sincos: dict = {}
+        self.checks: list = []
+
+    def new(self, expr: str) -> Sym:
+        got = self.memo.get(expr)
+        if got is not None:
+            return got
+        name = f"t{self.n}"
+        self.n += 1
+        self.lines.append(f"  const double {name} = {expr};")
+        s = Sym(name)
+        self.memo[expr] = s
+        return s
+
+    @staticmethod
+    def r(v) -> str:
+        if isinstance(v, Sym):
+            return v.name
+        if isinstance(v, Arr):
+            return lit(v.value)
+        return lit(v)
+
+    # -- arithmetic on symbolic values -----------------------------------
+    def bin(self, op, a, b):
+        sa, sb = isinstance(a, Sym), isinstance(b, Sym)
+        if not sa and not sb:
+            val = _fold(op, a.value if isinstance(a, Arr) else a, b.value if isinstance(b, Arr) else b)
+            return Arr(val) if (isinstance(a, Arr) or isinstance(b, Arr)) else val
+        # exact rewrites only
+        ca = None if sa else (a.value if isinstance(a, Arr) else float(a))
+        cb = None if sb else (b.value if isinstance(b, Arr) else float(b))
+        if op == "mul":
+            if cb == 1.0:
+                return a
+            if ca == 1.0:
+                return b
+            if cb == -1.0:
+                return self.neg(a)
+            if ca == -1.0:
+                return self.neg(b)
+        elif op == "div":
+            if cb == 1.0:
+                return a
+        elif op == "sub":
+            if cb == 0.0 and not math.copysign(1.0, cb) < 0:
+                return a
+        elif op == "add":
+            if cb == 0.0 and math.copysign(1.0, cb) < 0:
+                return a
+            if ca == 0.0 and math.copysign(1.0, ca) < 0:
+                return b
+        sym = {"add": "+", "sub": "-", "mul": "*", "div": "/"}[op]
+        return self.new(f"{self.r(a)} {sym} {self.r(b)}")
+
+    def add(self, a, b):
+        return self.bin("add", a, b)
+
+    def sub(self, a, b):
+        return self.bin("sub", a, b)
+
+    def mul(self, a, b):
+        return self.bin("mul", a, b)
+
+    def div(self, a, b):
+        return self.bin("div", a, b)
+
+    def neg(self, a):
+        if isinstance(a, Sym):
+            return self.new(f"-{a.name}")
+        if isinstance(a, Arr):
+            return Arr(-a.value)
+        return float(-np.float64(a))
+
+    def fn(self, name, a):
+        """np.<name>(a) for sin, cos, exp, log, sqrt."""
+        if not isinstance(a, Sym):
+            c = a.value if isinstance(a, Arr) else a
+            with np.errstate(all="ignore"):
+                val = float(getattr(np, name)(np.array([c], dtype=np.float64))[0])
+            return Arr(val) if isinstance(a, Arr) else val
+        if name in _SIN_COS:
+            pair = self.sincos.get(a.name)
+            if pair is None:
+                s, c = f"s_{a.name}", f"c_{a.name}"
+                self.lines.append(f"  double {s}, {c}; exa_sincos({a.name}, &{s}, &{c});")
+                pair = (Sym(s), Sym(c))
+                self.sincos[a.name] = pair
+            return pair[0] if name == "sin" else pair[1]
+        return self.new(f"{name}({a.name})")
+
+    def powi(self, a, n: int):
+        """np.power(a, n) for a Python int n (numpy: n=2 -> square, 1 -> copy,
+        0 -> ones, -1 -> reciprocal; measured bit-identical)."""
+        if not isinstance(a, Sym):
+            c = a.value if isinstance(a, Arr) else a
+            with np.errstate(all="ignore"):
+                val = float(np.power(np.array([c], dtype=np.float64), n)[0])
+            return Arr(val) if isinstance(a, Arr) else val
+        if n == 1:
+            return a
+        if n == 0:
+            return Arr(1.0)
+        if n == 2:
+            return self.new(f"{a.name} * {a.name}")
+        if n == -1:
+            return self.new(f"1.0 / {a.name}")
+        return self.new(f"exa_powi({a.name}, {int(n)})")
+
+    def pow(self, a, b):
+        if not isinstance(a, Sym) and not isinstance(b, Sym):
+            ca = a.value if isinstance(a, Arr) else a
+            cb = b.value if isinstance(b, Arr) else b
+            with np.errstate(all="ignore"):
+                val = float(np.power(np.array([ca]), np.array([cb]))[0])
+            return Arr(val) if (isinstance(a, Arr) or isinstance(b, Arr)) else val
+        return self.new(f"pow({self.r(a)}, {self.r(b)})")
+
+    # -- domain checks (values pass only) ----------------------------------
+    def check(self, kind, v, instr_idx):
+        """kind 'pos' (log/sqrt/pow) or 'nz' (div/ipow<0)."""
+        if isinstance(v, Sym):
+            cond = f"!({v.name} > 0.0)" if kind == "pos" else f"{v.name} == 0.0"
+            self.lines.append(f"  if ({cond}) EXA_DOMAIN({instr_idx});")
+            self.checks.append(instr_idx)
+        else:
+            c = v.value if isinstance(v, Arr) else v
+            bad = (not (c > 0.0)) if kind == "pos" else (c == 0.0)
+            if bad:
+                rec = "EXA_REC_ALL" if not isinstance(v, Arr) else "EXA_REC_FIRST"
+                self.lines.append(f"  EXA_DOMAIN_AT({instr_idx}, {rec});")
+                self.checks.append(instr_idx)
+
+
+class PatternCode:
+    """Generated source for one tape pattern plus what it needs at run time."""
+
+    def __init__(self, pid: int, tape, field_count: int, index_count: int, slot_struct):
+        self.pid = pid
+        self.tape = tape
+        self.nf = field_count
+        self.ni = index_count
+        self.slot_struct = slot_struct  # per slot: (block class, index column)
+        self.k = tape.k
+        self.has_checks = False
+        self.source = self._generate()
+
+    # ---------------------------------------------------------------- passes
+    def _values(self, g: Gen, loads):
+        v = [None] * len(self.instr)
+        for p, ins in enumerate(self.instr):
+            op = ins[0]
+            if op == "const":
+                v[p] = float(ins[1])
+            elif op == "field":
+                v[p] = loads["field"][ins[1]]
+            elif op == "var":
+                v[p] = loads["var"][ins[1]]
+            elif op == "neg":
+                v[p] = g.neg(v[ins[1]])
+            elif op in ("sin", "cos", "exp"):
+                v[p] = g.fn(op, v[ins[1]])
+            elif op in ("log", "sqrt"):
+                g.check("pos", v[ins[1]], p)
+                v[p] = g.fn(op, v[ins[1]])
+            elif op in ("add", "sub", "mul"):
+                v[p] = g.bin(op, v[ins[1]], v[ins[2]])
+            elif op == "div":
+                g.check("nz", v[ins[2]], p)
+                v[p] = g.div(v[ins[1]], v[ins[2]])
+            elif op == "ipow":
+                n = ins[2]
+                if n < 0:
+                    g.check("nz", v[ins[1]], p)
+                v[p] = g.mul(v[ins[1]], v[ins[1]]) if n == 2 else g.powi(v[ins[1]], n)
+            elif op == "pow":
+                g.check("pos", v[ins[1]], p)
+                v[p] = g.pow(v[ins[1]], v[ins[2]])
+            else:
+                raise ValueError(op)
+        return v
+
+    def _adjoints(self, g: Gen, v):
+        adj = [None] * len(self.instr)
+        adj[-1] = Arr(1.0)
+
+        def acc(at, val):
+            adj[at] = val if adj[at] is None else g.add(adj[at], val)
+
+        for p in range(len(self.instr) - 1, -1, -1):
+            a_p = adj[p]
+            ins = self.instr[p]
+            op = ins[0]
+            if a_p is None or op in ("const", "field", "var"):
+                continue
+            a = ins[1]
+            if op == "neg":
+                acc(a, g.neg(a_p))
+            elif op == "sin":
+                acc(a, g.mul(a_p, g.fn("cos", v[a])))
+            elif op == "cos":
+                acc(a, g.mul(g.neg(a_p), g.fn("sin", v[a])))
+            elif op == "exp":
+                acc(a, g.mul(a_p, v[p]))
+            elif op == "log":
+                acc(a, g.div(a_p, v[a]))
+            elif op == "sqrt":
+                acc(a, g.div(a_p, g.mul(2.0, v[p])))
+            elif op == "add":
+                acc(a, a_p)
+                acc(ins[2], a_p)
+            elif op == "sub":
+                acc(a, a_p)
+                acc(ins[2], g.neg(a_p))
+            elif op == "mul":
+                acc(a, g.mul(a_p, v[ins[2]]))
+                acc(ins[2], g.mul(a_p, v[a]))
+            elif op == "div":
+                b = ins[2]
+                acc(a, g.div(a_p, v[b]))
+                acc(b, g.div(g.mul(g.neg(a_p), v[p]), v[b]))
+            elif op == "ipow":
+                n = ins[2]
+                if n != 0:
+                    acc(a, g.mul(g.mul(a_p, float(n)), g.powi(v[a], n - 1)))
+            else:  # pow
+                b = ins[2]
+                acc(a, g.div(g.mul(g.mul(a_p, v[b]), v[p]), v[a]))
+                acc(b, g.mul(g.mul(a_p, v[p]), g.fn("log", v[a])))
+        return adj
+
+    def _slot_sums(self, g: Gen, per_node):
+        out = [Arr(0.0) for _ in range(self.k)]
+        for p, ins in enumerate(self.instr):
+            if ins[0] == "var" and per_node[p] is not None:
+                out[ins[1]] = g.add(out[ins[1]], per_node[p])
+        return out
+
+    def _tangents(self, g: Gen, v, seed):
+        Z = _is_zero
+        t = [0.0] * len(self.instr)
+        for p, ins in enumerate(self.instr):
+            op = ins[0]
+            if op == "var":
+                t[p] = 1.0 if ins[1] == seed else 0.0
+                continue
+            if op in ("const", "field"):
+                t[p] = 0.0
+                continue
+            ta = t[ins[1]]
+            if op == "neg":
+                t[p] = 0.0 if Z(ta) else g.neg(ta)
+            elif op == "sin":
+                t[p] = 0.0 if Z(ta) else g.mul(g.fn("cos", v[ins[1]]), ta)
+            elif op == "cos":
+                t[p] = 0.0 if Z(ta) else g.mul(g.neg(g.fn("sin", v[ins[1]])), ta)
+            elif op == "exp":
+                t[p] = 0.0 if Z(ta) else g.mul(v[p], ta)
+            elif op == "log":
+                t[p] = 0.0 if Z(ta) else g.div(ta, v[ins[1]])
+            elif op == "sqrt":
+                t[p] = 0.0 if Z(ta) else g.div(ta, g.mul(2.0, v[p]))
+            elif op == "add":
+                tb = t[ins[2]]
+                t[p] = tb if Z(ta) else (ta if Z(tb) else g.add(ta, tb))
+            elif op == "sub":
+                tb = t[ins[2]]
+                t[p] = ta if Z(tb) else (g.neg(tb) if Z(ta) else g.sub(ta, tb))
+            elif op == "mul":
+                tb = t[ins[2]]
+                lhs = 0.0 if Z(ta) else g.mul(ta, v[ins[2]])
+                rhs = 0.0 if Z(tb) else g.mul(v[ins[1]], tb)
+                t[p] = 0.0 if (Z(lhs) and Z(rhs)) else g.add(lhs, rhs)
+            elif op == "div":
+                tb = t[ins[2]]
+                if Z(ta) and Z(tb):
+                    t[p] = 0.0
+                else:
+                    lhs = 0.0 if Z(ta) else g.div(ta, v[ins[2]])
+                    rhs = 0.0 if Z(tb) else g.div(g.mul(v[p], tb), v[ins[2]])
+                    t[p] = g.sub(lhs, rhs)
+            elif op == "ipow":
+                n = ins[2]
+                if Z(ta) or n == 0:
+                    t[p] = 0.0
+                else:
+                    t[p] = g.mul(g.mul(float(n), g.powi(v[ins[1]], n - 1)), ta)
+            else:  # pow
+                tb = t[ins[2]]
+                if Z(ta) and Z(tb):
+                    t[p] = 0.0
+                else:
+                    base, ex = v[ins[1]], v[ins[2]]
+                    d = 0.0 if Z(ta) else g.div(g.mul(ex, ta), base)
+                    if not Z(tb):
+                        d = g.add(d, g.mul(g.fn("log", base), tb))
+                    t[p] = g.mul(v[p], d)
+        return t
+
+    def _adjoint_tangents(self, g: Gen, v, adj, t):
+        Z = _is_zero
+        dot = [None] * len(self.instr)
+        dot[-1] = 0.0
+
+        def accd(at, d_parent, partial, a_parent, partial_dot):
+            contrib = 0.0 if Z(d_parent) else g.mul(d_parent, partial)
+            if not Z(partial_dot):
+                contrib = g.add(contrib, g.mul(a_parent, partial_dot))
+            dot[at] = contrib if dot[at] is None else g.add(dot[at], contrib)
+
+        for p in range(len(self.instr) - 1, -1, -1):
+            a_p, d_p = adj[p], dot[p]
+            ins = self.instr[p]
+            op = ins[0]
+            if a_p is None or op in ("const", "field", "var"):
+                continue
+            a = ins[1]
+            if op == "neg":
+                accd(a, d_p, -1.0, a_p, 0.0)
+            elif op == "sin":
+                ta = t[a]
+                pd = 0.0 if Z(ta) else g.mul(g.neg(g.fn("sin", v[a])), ta)
+                accd(a, d_p, g.fn("cos", v[a]), a_p, pd)
+            elif op == "cos":
+                ta = t[a]
+                pd = 0.0 if Z(ta) else g.mul(g.neg(g.fn("cos", v[a])), ta)
+                accd(a, d_p, g.neg(g.fn("sin", v[a])), a_p, pd)
+            elif op == "exp":
+                accd(a, d_p, v[p], a_p, t[p])
+            elif op == "log":
+                ta = t[a]
+                pd = 0.0 if Z(ta) else g.div(g.neg(ta), g.mul(v[a], v[a]))
+                accd(a, d_p, g.div(1.0, v[a]), a_p, pd)
+            elif op == "sqrt":
+                tp = t[p]
+                pd = 0.0 if Z(tp) else g.div(g.neg(tp), g.mul(g.mul(2.0, v[p]), v[p]))
+                accd(a, d_p, g.div(1.0, g.mul(2.0, v[p])), a_p, pd)
+            elif op == "add":
+                accd(a, d_p, 1.0, a_p, 0.0)
+                accd(ins[2], d_p, 1.0, a_p, 0.0)
+            elif op == "sub":
+                accd(a, d_p, 1.0, a_p, 0.0)
+                accd(ins[2], d_p, -1.0, a_p, 0.0)
+            elif op == "mul":
+                b = ins[2]
+                accd(a, d_p, v[b], a_p, t[b])
+                accd(b, d_p, v[a], a_p, t[a])
+            elif op == "div":
+                b = ins[2]
+                den = v[b]
+                ta, tb = t[a], t[b]
+                pda = 0.0 if Z(tb) else g.div(g.neg(tb), g.mul(den, den))
+                if Z(ta) and Z(tb):
+                    pdb = 0.0
+                else:
+                    pdb = g.neg(0.0 if Z(ta) else g.div(ta, g.mul(den, den)))
+                    if not Z(tb):
+                        pdb = g.add(pdb, g.div(g.mul(g.mul(2.0, v[p]), tb), g.mul(den, den)))
+                accd(a, d_p, g.div(1.0, den), a_p, pda)
+                accd(b, d_p, g.div(g.neg(v[p]), den), a_p, pdb)
+            elif op == "ipow":
+                n = ins[2]
+                if n == 0:
+                    continue
+                base, ta = v[a], t[a]
+                part = g.mul(float(n), g.powi(base, n - 1))
+                if n <= 1 or Z(ta):
+                    pd = 0.0
+                else:
+                    pd = g.mul(g.mul(float(n * (n - 1)), g.powi(base, n - 2)), ta)
+                accd(a, d_p, part, a_p, pd)
+            else:  # pow
+                b = ins[2]
+                base, ex = v[a], v[b]
+                ta, tb, tp = t[a], t[b], t[p]
+                pa = g.div(g.mul(ex, v[p]), base)
+                pb = g.mul(v[p], g.fn("log", base))
+                pda = 0.0 if Z(tb) else g.div(g.mul(tb, v[p]), base)
+                if not Z(tp):
+                    pda = g.add(pda, g.div(g.mul(ex, tp), base))
+                if not Z(ta):
+                    pda = g.sub(pda, g.div(g.mul(g.mul(ex, v[p]), ta), g.mul(base, base)))
+                pdb = 0.0 if Z(tp) else g.mul(tp, g.fn("log", base))
+                if not Z(ta):
+                    pdb = g.add(pdb, g.div(g.mul(v[p], ta), base))
+                accd(a, d_p, pa, a_p, pda)
+                accd(b, d_p, pb, a_p, pdb)
+        return dot
+
+    # -------------------------------------------------------------- emission
+    def _generate(self) -> str:
+        self.instr = self.tape_norm()
+        k = self.k
+        g = Gen()
+        # loads: fields and gathered variables (each slot once)
+        loads = {"field": {}, "var": []}
+        pre = []
+        for fi, fname in enumerate(self.tape.field_names):
+            pre.append(f"  const double f{fi} = __ldg(T.f[{fi}] + r);")
+            loads["field"][fname] = Sym(f"f{fi}")
+        for ii in range(self.ni):
+            pre.append(f"  const int i{ii} = __ldg(T.ix[{ii}] + r);")
+        for s, (_, ic) in enumerate(self.slot_struct):
+            pre.append(f"  const int c{s} = T.voff[{s}] + i{ic};")
+            pre.append(f"  const double x{s} = __ldg(A.x + c{s});")
+            loads["var"].append(Sym(f"x{s}"))
+        v = self._values(g, loads)
+        value_lines = list(g.lines)
+        value_root = v[-1]
+        self.root_const = None if isinstance(value_root, (Sym, Arr)) else float(value_root)
+        self.has_checks = bool(g.checks)
+        n_value_lines = len(g.lines)
+
+        # first order
+        adj = self._adjoints(g, v) if k else None
+        grads = self._slot_sums(g, adj) if k else []
+        n_grad_lines = len(g.lines)
+        # second order: one forward-over-reverse sweep per seed slot
+        by_seed = []
+        for seed in range(k):
+            t = self._tangents(g, v, seed)
+            by_seed.append(self._slot_sums(g, self._adjoint_tangents(g, v, adj, t)))
+        body_grad = g.lines[n_value_lines:n_grad_lines]
+        body_hess = g.lines[n_grad_lines:]
+
+        out = []
+        pid = self.pid
+        R = Gen.r
+        # value-only function (row sums of augment-target rows, objective values)
+        out.append(f"__device__ __forceinline__ double exa_val_{pid}(const ExaTerm& T, int r, const ExaArgs& A, int rank) {{")
+        out.extend(pre)
+        out.extend(value_lines)
+        out.append(f"  return {R(value_root)};")
+        out.append("}")
+
+        # full term function, MODE-templated; unused temps are dead code
+        out.append(f"template <int MODE>\n__device__ __forceinline__ void exa_term_{pid}(const ExaTerm& T, int r, const ExaArgs& A, int rank) {{")
+        out.extend(pre)
+        out.extend(value_lines)
+        out.append("  if (MODE & (EXA_M_CONS | EXA_M_OBJV)) {")
+        out.append(f"    const double root = {R(value_root)};")
+        out.append("    if ((MODE & EXA_M_CONS) && T.cons_direct) A.c[T.row_offset + r] = 0.0 + root;")
+        out.append("    if ((MODE & EXA_M_OBJV) && T.kind == EXA_OBJ) A.V[T.scr0 + r] = root;")
+        out.append("  }")
+        if k:
+            out.append("  if (MODE & (EXA_M_JAC | EXA_M_GRAD | EXA_M_HESS)) {")
+            out.extend("  " + l for l in body_grad)
+            out.append("    if ((MODE & EXA_M_JAC) && T.kind != EXA_OBJ) {")
+            for s in range(k):
+                out.append(f"      A.J[T.jac0 + {s}LL * T.nrec + r] = {R(grads[s])};")
+            out.append("    }")
+            out.append("    if ((MODE & EXA_M_GRAD) && T.kind == EXA_OBJ) {")
+            for s in range(k):
+                out.append(f"      A.G[T.scr0 + {s}LL * T.nrec + r] = {R(grads[s])};")
+            out.append("    }")
+            out.append("    if (MODE & EXA_M_HESS) {")
+            out.append("      const double wgt = (T.kind == EXA_OBJ) ? A.w : __ldg(A.y + (T.rows ? __ldg(T.rows + r) : T.row_offset + r));")
+            out.extend("    " + l for l in body_hess)
+            pair = 0
+            for i in range(k):
+                for j in range(i + 1):
+                    val = by_seed[j][i]
+                    expr = R(val)
+                    bi, bj = self.slot_struct[i][0], self.slot_struct[j][0]
+                    if i != j and bi == bj:
+                        expr = f"(c{i} == c{j} ? {expr} * 2.0 : {expr})"
+                    out.append(f"      A.H[T.hess0 + {pair}LL * T.nrec + r] = wgt * {expr};")
+                    pair += 1
+            out.append("    }")
+            out.append("  }")
+        out.append("}")
+        return "\n".join(out)
+
+    def tape_norm(self):
+        return list(self.tape.instr)

@@ -1,0 +1,534 @@
+// exa_capi.cu -- libexa.so: C ABI, plan management, NVRTC JIT, and the static
+// aggregation kernels of the B200 callback engine.  See include/exa.h.
+//
+// Static kernels here (the generated per-model kernels live in the JIT module):
+//   exa_obj_leaves / exa_obj_combine  objective sum in numpy's pairwise order
+//                                      (reference eval_objective, autodiff.py:536-547)
+//   exa_grad_reduce                    dense gradient, bincount order per variable
+//                                      (reference eval_gradient, autodiff.py:550-563)
+//   exa_compress_reduce                CompressedPattern.sum_values (autodiff.py:672-674)
+//   exa_sincos_kernel                  device check of exa_sincos (diagnostics)
+// All reductions are sequential per output element in the reference's order:
+// deterministic, no floating-point atomics.
+
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/exa.h"
+#include "exa_device.h"
+#include "exa_math.h"
+
+static_assert(sizeof(ExaSegDesc) == sizeof(ExaSeg), "segment layout");
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return -1;
+}
+
+#define CU(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess) return fail("%s failed: %s", #call, cudaGetErrorString(e_));      \
+  } while (0)
+
+template <class T>
+int dev_upload(T** dst, const T* src, size_t n) {
+  *dst = nullptr;
+  if (n == 0) return 0;
+  CU(cudaMalloc((void**)dst, n * sizeof(T)));
+  CU(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+const char* kKernelNames[EXA_NMODES] = {"exa_k_set", "exa_k_cons", "exa_k_jac",
+                                        "exa_k_hess", "exa_k_objv", "exa_k_grad"};
+
+// objective combine program opcodes (see paper_2510_12897_b200/device.py)
+enum { OP_LEAF = 0, OP_ADD = 1, OP_CONST = 2, OP_ZERO_PLUS = 3, OP_TOTAL_ADD = 4 };
+
+}  // namespace
+
+struct ExaWorkspace {
+  ExaPlan* plan = nullptr;
+  double* V = nullptr;
+  double* G = nullptr;
+  double* leafsum = nullptr;
+  unsigned long long* err = nullptr;
+};
+
+struct ExaPlan {
+  int device = 0;
+  int64_t nvar = 0, ncon = 0, n_jac = 0, n_hess = 0;
+  int threads = 256;
+  double* f64 = nullptr;
+  int32_t* i32 = nullptr;
+  ExaTerm* terms = nullptr;
+  int32_t n_terms = 0;
+  ExaSeg* segs[EXA_NMODES] = {};
+  int* cta_seg[EXA_NMODES] = {};
+  int n_ctas[EXA_NMODES] = {};
+  int err_base[EXA_NMODES][2] = {};
+  int64_t n_vscr = 0, n_gscr = 0;
+  int64_t* leaves = nullptr;
+  int32_t n_leaves = 0;
+  int64_t* prog = nullptr;
+  int32_t n_prog = 0;
+  int64_t* grad_ptr = nullptr;
+  int64_t* grad_ent = nullptr;
+  int has_checks = 0;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern[EXA_NMODES] = {};
+  ExaWorkspace* dflt = nullptr;
+  size_t bytes = 0;
+};
+
+// ---------------------------------------------------------------------------
+// static kernels
+// ---------------------------------------------------------------------------
+
+// One leaf of numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src
+// pairwise_sum): n < 8 -> plain loop; 8 <= n <= 128 -> 8 strided accumulators,
+// combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail.
+__global__ void exa_obj_leaves(const double* __restrict__ V, const int64_t* __restrict__ leaves,
+                               int n_leaves, double* __restrict__ out) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= n_leaves) return;
+  const double* a = V + leaves[2 * l];
+  const int64_t n = leaves[2 * l + 1];
+  double res;
+  if (n < 8) {
+    res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res = res + a[i];
+  } else {
+    double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8) {
+      r0 = r0 + a[i + 0];
+      r1 = r1 + a[i + 1];
+      r2 = r2 + a[i + 2];
+      r3 = r3 + a[i + 3];
+      r4 = r4 + a[i + 4];
+      r5 = r5 + a[i + 5];
+      r6 = r6 + a[i + 6];
+      r7 = r7 + a[i + 7];
+    }
+    res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+    for (; i < n; ++i) res = res + a[i];
+  }
+  out[l] = res;
+}
+
+// The pairwise tree above the leaves plus the Python-level `total += s_t`
+// accumulation over objective blocks, replayed by one thread.
+__global__ void exa_obj_combine(const int64_t* __restrict__ prog, int n_prog,
+                                const double* __restrict__ leafsum, double* __restrict__ out) {
+  double stack[96];
+  int sp = 0;
+  double total = 0.0;
+  for (int p = 0; p < n_prog; ++p) {
+    const int64_t op = prog[3 * p], a = prog[3 * p + 1];
+    switch ((int)op) {
+      case OP_LEAF: stack[sp++] = leafsum[a]; break;
+      case OP_ADD: {
+        const double b = stack[--sp];
+        const double x = stack[--sp];
+        stack[sp++] = x + b;
+        break;
+      }
+      case OP_CONST: stack[sp++] = __longlong_as_double((long long)a); break;
+      case OP_ZERO_PLUS: stack[sp - 1] = 0.0 + stack[sp - 1]; break;
+      case OP_TOTAL_ADD: total = total + stack[--sp]; break;
+      default: break;
+    }
+    if (sp >= 96) sp = 95;  // malformed program guard
+  }
+  *out = total;
+}
+
+// g[v] = ((0 + B_1) + B_2) + ..., B_k = sequential bincount sum of group k.
+__global__ void exa_grad_reduce(int64_t nvar, const int64_t* __restrict__ ptr, const int64_t* __restrict__ ent,
+                                const double* __restrict__ G, double* __restrict__ g) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvar) return;
+  double acc = 0.0, grp = 0.0;
+  bool open = false;
+  const int64_t e1 = ptr[v + 1];
+  for (int64_t e = ptr[v]; e < e1; ++e) {
+    const int64_t en = ent[e];
+    if (en >> 62) {
+      if (open) acc = acc + grp;
+      grp = 0.0;
+      open = true;
+    }
+    grp = grp + G[en & ((1LL << 62) - 1)];
+  }
+  if (open) acc = acc + grp;
+  g[v] = acc;
+}
+
+// compressed[k] = 0 + sum of raw slots mapped to k, in slot order (np.bincount).
+__global__ void exa_compress_reduce(int64_t nnz, const int64_t* __restrict__ ptr, const int32_t* __restrict__ ent,
+                                    const double* __restrict__ raw, double* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+  double acc = 0.0;
+  const int64_t e1 = ptr[k + 1];
+  for (int64_t e = ptr[k]; e < e1; ++e) acc = acc + __ldg(raw + __ldg(ent + e));
+  out[k] = acc;
+}
+
+__global__ void exa_sincos_kernel(const double* __restrict__ x, double* __restrict__ s, double* __restrict__ c,
+                                  int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double sv, cv;
+  exa_sincos(x[i], &sv, &cv);
+  s[i] = sv;
+  c[i] = cv;
+}
+
+static inline unsigned grid_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* exa_last_error(void) { return g_err.c_str(); }
+
+void exa_free(void* p) { free(p); }
+
+int exa_nvrtc_version(int* major, int* minor) {
+  if (nvrtcVersion(major, minor) != NVRTC_SUCCESS) return fail("nvrtcVersion failed");
+  return 0;
+}
+
+int exa_jit_compile(const char* src, const char* name, const char* const* opts, int n_opts, void** cubin,
+                    size_t* cubin_size, char** log) {
+  if (!src || !cubin || !cubin_size) return fail("exa_jit_compile: null argument");
+  *cubin = nullptr;
+  *cubin_size = 0;
+  if (log) *log = nullptr;
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, src, name ? name : "exa_gen.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return fail("nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
+  r = nvrtcCompileProgram(prog, n_opts, opts);
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  std::string lg(log_size, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, &lg[0]);
+  if (log && log_size > 1) {
+    *log = (char*)malloc(log_size);
+    memcpy(*log, lg.data(), log_size);
+  }
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return fail("NVRTC compile failed: %s\n%.4000s", nvrtcGetErrorString(r), lg.c_str());
+  }
+  size_t n = 0;
+  if (nvrtcGetCUBINSize(prog, &n) != NVRTC_SUCCESS || n == 0) {
+    nvrtcDestroyProgram(&prog);
+    return fail("nvrtcGetCUBINSize failed (was -arch=sm_100a given?)");
+  }
+  void* buf = malloc(n);
+  nvrtcGetCUBIN(prog, (char*)buf);
+  nvrtcDestroyProgram(&prog);
+  *cubin = buf;
+  *cubin_size = n;
+  return 0;
+}
+
+static int ws_alloc(ExaPlan* p, ExaWorkspace** out) {
+  ExaWorkspace* w = new ExaWorkspace();
+  w->plan = p;
+  if (p->n_vscr) CU(cudaMalloc((void**)&w->V, p->n_vscr * sizeof(double)));
+  if (p->n_gscr) CU(cudaMalloc((void**)&w->G, p->n_gscr * sizeof(double)));
+  if (p->n_leaves) CU(cudaMalloc((void**)&w->leafsum, p->n_leaves * sizeof(double)));
+  CU(cudaMalloc((void**)&w->err, sizeof(unsigned long long)));
+  CU(cudaMemset(w->err, 0xff, sizeof(unsigned long long)));
+  *out = w;
+  return 0;
+}
+
+void exa_workspace_destroy(ExaWorkspace* w) {
+  if (!w) return;
+  cudaFree(w->V);
+  cudaFree(w->G);
+  cudaFree(w->leafsum);
+  cudaFree(w->err);
+  delete w;
+}
+
+int exa_workspace_create(ExaPlan* p, ExaWorkspace** out) {
+  if (!p || !out) return fail("exa_workspace_create: null argument");
+  CU(cudaSetDevice(p->device));
+  return ws_alloc(p, out);
+}
+
+void exa_plan_destroy(ExaPlan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  exa_workspace_destroy(p->dflt);
+  cudaFree(p->f64);
+  cudaFree(p->i32);
+  cudaFree(p->terms);
+  for (int m = 0; m < EXA_NMODES; ++m) {
+    cudaFree(p->segs[m]);
+    cudaFree(p->cta_seg[m]);
+  }
+  cudaFree(p->leaves);
+  cudaFree(p->prog);
+  cudaFree(p->grad_ptr);
+  cudaFree(p->grad_ent);
+  if (p->lib) cudaLibraryUnload(p->lib);
+  delete p;
+}
+
+int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
+  if (!d || !out) return fail("exa_plan_create: null argument");
+  *out = nullptr;
+  if (d->abi_version != EXA_ABI_VERSION) return fail("ABI version %d != %d", d->abi_version, EXA_ABI_VERSION);
+  if (!d->cubin || d->cubin_size <= 0) return fail("exa_plan_create: no kernel module");
+  CU(cudaSetDevice(d->device));
+  ExaPlan* p = new ExaPlan();
+  int rc = 0;
+  auto bail = [&](int code) {
+    exa_plan_destroy(p);
+    return code;
+  };
+  p->device = d->device;
+  p->nvar = d->nvar;
+  p->ncon = d->ncon;
+  p->n_jac = d->n_jac;
+  p->n_hess = d->n_hess;
+  p->threads = d->threads > 0 ? d->threads : 256;
+  p->n_terms = d->n_terms;
+  p->has_checks = d->has_domain_checks;
+  p->n_vscr = d->n_vscr;
+  p->n_gscr = d->n_gscr;
+  if ((rc = dev_upload(&p->f64, d->f64, (size_t)d->n_f64))) return bail(rc);
+  if ((rc = dev_upload(&p->i32, d->i32, (size_t)d->n_i32))) return bail(rc);
+  p->bytes += d->n_f64 * 8 + d->n_i32 * 4;
+
+  // terms: translate blob offsets into device pointers
+  std::vector<ExaTerm> terms(d->n_terms);
+  for (int t = 0; t < d->n_terms; ++t) {
+    const ExaTermDesc& s = d->terms[t];
+    ExaTerm& T = terms[t];
+    memset(&T, 0, sizeof T);
+    for (int i = 0; i < EXA_MAXF; ++i) T.f[i] = s.f_off[i] >= 0 ? p->f64 + s.f_off[i] : nullptr;
+    for (int i = 0; i < EXA_MAXI; ++i) T.ix[i] = s.ix_off[i] >= 0 ? p->i32 + s.ix_off[i] : nullptr;
+    T.rows = s.rows_off >= 0 ? p->i32 + s.rows_off : nullptr;
+    T.row_ptr = s.row_ptr_off >= 0 ? p->i32 + s.row_ptr_off : nullptr;
+    T.row_ent = s.row_ent_off >= 0 ? reinterpret_cast<const int2*>(p->i32 + s.row_ent_off) : nullptr;
+    for (int i = 0; i < EXA_MAXK; ++i) T.voff[i] = s.voff[i];
+    T.nrec = s.nrec;
+    T.pattern = s.pattern;
+    T.kind = s.kind;
+    T.order = s.order;
+    T.row_offset = s.row_offset;
+    T.cons_direct = s.cons_direct;
+    T.k = s.k;
+    T.jac0 = s.jac0;
+    T.hess0 = s.hess0;
+    T.scr0 = s.scr0;
+    if (s.row_ent_off >= 0 && (s.row_ent_off & 1)) return bail(fail("term %d: row entries misaligned", t));
+  }
+  if ((rc = dev_upload(&p->terms, terms.data(), terms.size()))) return bail(rc);
+  p->bytes += terms.size() * sizeof(ExaTerm);
+
+  for (int m = 0; m < EXA_NMODES; ++m) {
+    const int ns = d->n_segs[m];
+    p->n_ctas[m] = d->n_ctas[m];
+    p->err_base[m][0] = d->err_base[m][0];
+    p->err_base[m][1] = d->err_base[m][1];
+    if (ns == 0) continue;
+    if ((rc = dev_upload(&p->segs[m], reinterpret_cast<const ExaSeg*>(d->segs[m]), (size_t)ns))) return bail(rc);
+    std::vector<int> map(d->n_ctas[m], -1);
+    for (int s = 0; s < ns; ++s) {
+      const ExaSegDesc& sg = d->segs[m][s];
+      const int nc = (sg.nrec + p->threads - 1) / p->threads;
+      for (int c = 0; c < nc; ++c) {
+        if (sg.cta0 + c >= d->n_ctas[m]) return bail(fail("mode %d: segment %d overflows the grid", m, s));
+        map[sg.cta0 + c] = s;
+      }
+    }
+    for (int c = 0; c < d->n_ctas[m]; ++c)
+      if (map[c] < 0) return bail(fail("mode %d: CTA %d has no segment", m, c));
+    if ((rc = dev_upload(&p->cta_seg[m], map.data(), map.size()))) return bail(rc);
+    p->bytes += ns * sizeof(ExaSeg) + map.size() * sizeof(int);
+  }
+
+  p->n_leaves = d->n_leaves;
+  p->n_prog = d->n_prog;
+  if ((rc = dev_upload(&p->leaves, d->leaves, (size_t)d->n_leaves * 2))) return bail(rc);
+  if ((rc = dev_upload(&p->prog, d->obj_prog, (size_t)d->n_prog * 3))) return bail(rc);
+  if (d->grad_ptr) {
+    if ((rc = dev_upload(&p->grad_ptr, d->grad_ptr, (size_t)d->nvar + 1))) return bail(rc);
+    if ((rc = dev_upload(&p->grad_ent, d->grad_ent, (size_t)d->n_grad_ent))) return bail(rc);
+  }
+
+  cudaError_t e = cudaLibraryLoadData(&p->lib, d->cubin, nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e != cudaSuccess) return bail(fail("cudaLibraryLoadData: %s", cudaGetErrorString(e)));
+  for (int m = 0; m < EXA_NMODES; ++m) {
+    e = cudaLibraryGetKernel(&p->kern[m], p->lib, kKernelNames[m]);
+    if (e != cudaSuccess) return bail(fail("cudaLibraryGetKernel(%s): %s", kKernelNames[m], cudaGetErrorString(e)));
+  }
+  if ((rc = ws_alloc(p, &p->dflt))) return bail(rc);
+  *out = p;
+  return 0;
+}
+
+int exa_plan_info(const ExaPlan* p, int64_t* bytes, int32_t* regs) {
+  if (!p) return fail("exa_plan_info: null plan");
+  if (bytes) *bytes = (int64_t)p->bytes;
+  if (regs) {
+    cudaFuncAttributes a;
+    CU(cudaFuncGetAttributes(&a, (const void*)p->kern[EXA_MODE_SET]));
+    *regs = a.numRegs;
+  }
+  return 0;
+}
+
+static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaStream_t st) {
+  if (p->n_ctas[mode] == 0) return 0;
+  A.err = w->err;
+  A.obj_base = p->err_base[mode][0];
+  A.con_base = p->err_base[mode][1];
+  const ExaTerm* terms = p->terms;
+  const ExaSeg* segs = p->segs[mode];
+  const int* cmap = p->cta_seg[mode];
+  void* args[] = {(void*)&terms, (void*)&segs, (void*)&cmap, (void*)&A};
+  CU(cudaLaunchKernel((const void*)p->kern[mode], dim3(p->n_ctas[mode]), dim3(p->threads), args, 0, st));
+  return 0;
+}
+
+static int reset_err(ExaPlan* p, ExaWorkspace* w, cudaStream_t st) {
+  if (p->has_checks) CU(cudaMemsetAsync(w->err, 0xff, sizeof(unsigned long long), st));
+  return 0;
+}
+
+#define EXA_PROLOGUE()                                      \
+  if (!p) return fail("null plan");                         \
+  ExaWorkspace* w = ws ? ws : p->dflt;                      \
+  cudaStream_t st = (cudaStream_t)stream;                   \
+  ExaArgs A;                                                \
+  memset(&A, 0, sizeof A);                                  \
+  if (int rc_ = reset_err(p, w, st)) return rc_;
+
+int exa_eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
+                 double* jac, double* hess, exa_stream_t stream) {
+  EXA_PROLOGUE();
+  A.x = x;
+  A.y = mult;
+  A.w = w_obj;
+  A.c = c;
+  A.J = jac;
+  A.H = hess;
+  return launch_mode(p, w, EXA_MODE_SET, A, st);
+}
+
+int exa_eval_cons(ExaPlan* p, ExaWorkspace* ws, const double* x, double* c, exa_stream_t stream) {
+  EXA_PROLOGUE();
+  A.x = x;
+  A.c = c;
+  return launch_mode(p, w, EXA_MODE_CONS, A, st);
+}
+
+int exa_eval_jac(ExaPlan* p, ExaWorkspace* ws, const double* x, double* jac, exa_stream_t stream) {
+  EXA_PROLOGUE();
+  A.x = x;
+  A.J = jac;
+  return launch_mode(p, w, EXA_MODE_JAC, A, st);
+}
+
+int exa_eval_hess(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj,
+                  double* hess, exa_stream_t stream) {
+  EXA_PROLOGUE();
+  A.x = x;
+  A.y = mult;
+  A.w = w_obj;
+  A.H = hess;
+  return launch_mode(p, w, EXA_MODE_HESS, A, st);
+}
+
+int exa_eval_obj(ExaPlan* p, ExaWorkspace* ws, const double* x, double* out, exa_stream_t stream) {
+  EXA_PROLOGUE();
+  A.x = x;
+  A.V = w->V;
+  int rc = launch_mode(p, w, EXA_MODE_OBJV, A, st);
+  if (rc) return rc;
+  if (p->n_leaves) {
+    exa_obj_leaves<<<grid_for(p->n_leaves, 128), 128, 0, st>>>(w->V, p->leaves, p->n_leaves, w->leafsum);
+    CU(cudaGetLastError());
+  }
+  exa_obj_combine<<<1, 1, 0, st>>>(p->prog, p->n_prog, w->leafsum, out);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int exa_eval_grad(ExaPlan* p, ExaWorkspace* ws, const double* x, double* g, exa_stream_t stream) {
+  EXA_PROLOGUE();
+  A.x = x;
+  A.G = w->G;
+  int rc = launch_mode(p, w, EXA_MODE_GRAD, A, st);
+  if (rc) return rc;
+  if (p->nvar) {
+    if (p->grad_ptr) {
+      exa_grad_reduce<<<grid_for(p->nvar, 256), 256, 0, st>>>(p->nvar, p->grad_ptr, p->grad_ent, w->G, g);
+      CU(cudaGetLastError());
+    } else {
+      CU(cudaMemsetAsync(g, 0, p->nvar * sizeof(double), st));
+    }
+  }
+  return 0;
+}
+
+int exa_segment_sum(int64_t nnz, const int64_t* ptr, const int32_t* ent, const double* raw, double* out,
+                    exa_stream_t stream) {
+  if (nnz <= 0) return 0;
+  if (!ptr || !ent || !raw || !out) return fail("exa_segment_sum: null argument");
+  exa_compress_reduce<<<grid_for(nnz, 256), 256, 0, (cudaStream_t)stream>>>(nnz, ptr, ent, raw, out);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int exa_domain_error(ExaPlan* p, ExaWorkspace* ws, exa_stream_t stream, int64_t* rank, int32_t* instr,
+                     int64_t* record) {
+  if (!p) return fail("null plan");
+  if (!p->has_checks) return 0;
+  ExaWorkspace* w = ws ? ws : p->dflt;
+  unsigned long long key = 0;
+  CU(cudaMemcpyAsync(&key, w->err, sizeof key, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CU(cudaStreamSynchronize((cudaStream_t)stream));
+  if (key == EXA_ERR_NONE) return 0;
+  if (rank) *rank = (int64_t)(key >> 44);
+  if (instr) *instr = (int32_t)((key >> 32) & 0xfff);
+  if (record) *record = (int64_t)(key & 0xffffffffull) - 1;
+  return 1;
+}
+
+int exa_device_sincos(const double* x, double* s, double* c, int64_t n, exa_stream_t stream) {
+  if (n <= 0) return 0;
+  exa_sincos_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, s, c, n);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+}  // extern "C"

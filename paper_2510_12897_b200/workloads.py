@@ -1,0 +1,78 @@
+"""Benchmark workloads (BASELINE.json configs) and their algorithmic bytes.
+
+Configs:
+
+* ``case14``      bundled-style small case (parity; CPU-runnable reference);
+* ``case1354``    pglib case1354_pegase-shaped, polar, static;
+* ``case13659``   pglib case13659_pegase-shaped, polar, static (headline);
+* ``mp96_case1354``  96-period MPOPF with ramping on the 1354-shaped network;
+* ``n1_case2000``    N-1 batch on the case2000-shaped network (see :mod:`.scopf`).
+
+``algorithmic_bytes`` is SURVEY §8(d)'s compulsory-traffic count for one
+callback set (cons + jac + hess): x and y once, every term parameter once
+(fp64 fields, int32 index columns, +1 int32 row column for augments), every
+output once.  COO structure arrays are not re-read per set.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .opf import mpopf_model, opf_model
+from .synth import demand_curve, pglib_shaped
+
+WORKLOADS = ("case14", "case1354", "case2000", "case13659", "mp96_case1354")
+
+
+def build_workload(name: str, lower_to_gpu: bool = True, seed: int = 1):
+    if name in ("case14", "case1354", "case2000", "case13659"):
+        case = pglib_shaped(name, seed=seed)
+        return opf_model(case, form="polar", lower_to_gpu=lower_to_gpu)[0]
+    if name.startswith("mp"):
+        T = int(name[2:].split("_")[0])
+        case = pglib_shaped(name.split("_", 1)[1], seed=seed)
+        return mpopf_model(case, demand_curve(T), corrective_action_ratio=0.25, form="polar",
+                           lower_to_gpu=lower_to_gpu)[0]
+    raise KeyError(name)
+
+
+def algorithmic_bytes(model) -> dict:
+    plan = model.plan
+    params = 0
+    for tp in plan.obj_terms + plan.con_terms:
+        n_idx = len(tp.tape.index_names) + (1 if tp.kind == "augment" else 0)
+        params += tp.nrec * (8 * len(tp.tape.field_names) + 4 * n_idx)
+    parts = {
+        "x": 8 * model.nvar,
+        "y": 8 * model.ncon,
+        "params": params,
+        "cons": 8 * model.ncon,
+        "jac": 8 * plan.n_jac_slots,
+        "hess": 8 * plan.n_hess_slots,
+    }
+    parts["total"] = sum(parts.values())
+    return parts
+
+
+def bench_models_for_precompile():
+    """Host plans whose kernel modules build() pre-compiles (no GPU needed)."""
+    out = []
+    for name in ("case13659", "mp96_case1354"):
+        out.append(build_workload(name, lower_to_gpu=False).plan)
+    return out
+
+
+def model_summary(model) -> dict:
+    b = algorithmic_bytes(model)
+    return {
+        "nvar": model.nvar, "ncon": model.ncon,
+        "jac_slots": model.plan.n_jac_slots, "hess_slots": model.plan.n_hess_slots,
+        "bytes_per_set": b["total"], "bytes": b,
+    }
+
+
+def eval_inputs(model, seed: int = 0):
+    from .synth import evaluation_point
+
+    x, y, w = evaluation_point(model, seed)
+    return np.ascontiguousarray(x), np.ascontiguousarray(y), w
