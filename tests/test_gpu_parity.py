@@ -177,7 +177,7 @@ def test_device_sincos_is_correctly_rounded_and_matches_host_build():
     torch.cuda.synchronize()
     hs, hc = crtrig.sincos(x)
     # beyond |x| = 2^20 pi/2 both sides fall back to their platform libm
-    dd = ~(np.abs(x) > 0x1.921fb54442d18p+20)
+    dd = ~(np.abs(x) > float.fromhex("0x1.921fb54442d18p+20"))
     assert bitwise_equal(s.cpu().numpy()[dd], hs[dd]) and bitwise_equal(c.cpu().numpy()[dd], hc[dd])
     # vs glibc: only 1-ulp differences, on a small fraction of arguments
     fin = np.isfinite(x) & (np.abs(x) < 1e5)
