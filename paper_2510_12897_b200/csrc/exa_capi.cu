@@ -83,6 +83,7 @@ struct ExaPlan {
   ExaSeg* segs[EXA_NMODES] = {};
   int* cta_seg[EXA_NMODES] = {};
   int n_ctas[EXA_NMODES] = {};
+  int n_segs_mode[EXA_NMODES] = {};
   int err_base[EXA_NMODES][2] = {};
   int64_t n_vscr = 0, n_gscr = 0;
   int64_t* leaves = nullptr;
@@ -96,6 +97,8 @@ struct ExaPlan {
   cudaKernel_t kern[EXA_NMODES] = {};
   ExaWorkspace* dflt = nullptr;
   size_t bytes = 0;
+  int seg_off[EXA_NMODES] = {};
+  bool meta_const = false;
 };
 
 // ---------------------------------------------------------------------------
@@ -355,6 +358,7 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
 
   for (int m = 0; m < EXA_NMODES; ++m) {
     const int ns = d->n_segs[m];
+    p->n_segs_mode[m] = ns;
     p->n_ctas[m] = d->n_ctas[m];
     p->err_base[m][0] = d->err_base[m][0];
     p->err_base[m][1] = d->err_base[m][1];
@@ -390,6 +394,28 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
     e = cudaLibraryGetKernel(&p->kern[m], p->lib, kKernelNames[m]);
     if (e != cudaSuccess) return bail(fail("cudaLibraryGetKernel(%s): %s", kKernelNames[m], cudaGetErrorString(e)));
   }
+  // Constant-memory metadata variant: the module declares exa_terms_c /
+  // exa_segs_c; fill them with the term table and all callbacks' segments.
+  {
+    void* cterms = nullptr;
+    void* csegs = nullptr;
+    size_t nb_t = 0, nb_s = 0;
+    if (cudaLibraryGetGlobal(&cterms, &nb_t, p->lib, "exa_terms_c") == cudaSuccess &&
+        cudaLibraryGetGlobal(&csegs, &nb_s, p->lib, "exa_segs_c") == cudaSuccess) {
+      std::vector<ExaSeg> all;
+      for (int m = 0; m < EXA_NMODES; ++m) {
+        p->seg_off[m] = (int)all.size();
+        for (int s = 0; s < d->n_segs[m]; ++s) all.push_back(reinterpret_cast<const ExaSeg*>(d->segs[m])[s]);
+      }
+      if (terms.size() * sizeof(ExaTerm) > nb_t || all.size() * sizeof(ExaSeg) > nb_s)
+        return bail(fail("model too large for the constant-metadata module variant"));
+      CU(cudaMemcpy(cterms, terms.data(), terms.size() * sizeof(ExaTerm), cudaMemcpyHostToDevice));
+      if (!all.empty()) CU(cudaMemcpy(csegs, all.data(), all.size() * sizeof(ExaSeg), cudaMemcpyHostToDevice));
+      p->meta_const = true;
+    } else {
+      cudaGetLastError();  // clear the lookup failure
+    }
+  }
   if ((rc = ws_alloc(p, &p->dflt))) return bail(rc);
   *out = p;
   return 0;
@@ -411,6 +437,11 @@ static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaSt
   A.err = w->err;
   A.obj_base = p->err_base[mode][0];
   A.con_base = p->err_base[mode][1];
+  A.seg_off = p->seg_off[mode];
+  A.f64 = p->f64;
+  A.i32 = p->i32;
+  A.n_segs = 0;
+  A.n_segs = p->n_segs_mode[mode];
   const ExaTerm* terms = p->terms;
   const ExaSeg* segs = p->segs[mode];
   const int* cmap = p->cta_seg[mode];

@@ -27,14 +27,20 @@
 
 /* segment kinds */
 #define EXA_SEG_TERM 0
-#define EXA_SEG_ROW 1
+#define EXA_SEG_ROW 1  /* one thread per row, serial CSR loop (rows > 32 entries) */
+#define EXA_SEG_FOLD 2 /* warp-parallel row sums: one lane per contribution     */
+
+/* constant-memory metadata limits (models beyond them use global memory) */
+#define EXA_CMAX_TERMS 96
+#define EXA_CMAX_SEGS 1024
 
 typedef struct ExaTerm {
   const double* f[EXA_MAXF]; /* real field columns, normalised order     */
   const int* ix[EXA_MAXI];   /* index columns, normalised order           */
   const int* rows;           /* augment rows (global row ids) or 0        */
-  const int* row_ptr;        /* augment-target base block: CSR over rows   */
-  const int2* row_ent;       /*   entries (term, record), reference order */
+  const int* row_ptr;        /* augment-target block, serial mode: CSR over rows */
+  const int2* row_ent;       /*   serial: (term, record) per CSR entry;
+                                  fold: padded slots (term | pos<<16, record), -1 = pad */
   int voff[EXA_MAXK];        /* variable-block offset of each slot        */
   int nrec;
   int pattern;
@@ -68,6 +74,10 @@ typedef struct ExaArgs {
   unsigned long long* err; /* domain-error key, atomicMin */
   int obj_base; /* domain-error rank offset of objective terms in this callback */
   int con_base; /* ... and of constraint-side terms */
+  int seg_off;  /* this callback's segments in the constant segment table */
+  int n_segs;
+  const double* f64; /* plan blobs (model-specialised modules address terms */
+  const int* i32;    /*   as blob + compile-time offsets)                    */
 } ExaArgs;
 
 /* domain-error key: order (20 bits) | instr (12 bits) | record+1 (32 bits) */

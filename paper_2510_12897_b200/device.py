@@ -5,15 +5,18 @@ HBM layout (one plan, read-only after creation):
 * ``f64`` blob -- every real field column of every term, SoA, each column
   256-byte aligned (reference ``DataTable.reals``, ``core.py:36-64``);
 * ``i32`` blob -- index columns as int32 in-block positions, augment row
-  columns, the CSR of augment contributions per balance row;
-* term table -- one :c:type:`ExaTerm` per term (pointers into the blobs,
-  per-slot block offsets, output starts in the raw J/H layouts);
-* per-callback segment tables -- CTA -> (term, records) maps so that each
+  columns, the per-row contribution lists of augment-target blocks;
+* term table -- one :c:type:`ExaTerm` per term (blob offsets, per-slot block
+  offsets, output starts in the raw J/H layouts);
+* per-callback segment tables -- CTA -> (term, records) so that each
   callback is ONE launch of the model's generated kernel.
 
 Outputs are caller buffers: raw Jacobian ``[term][slot][record]`` and raw
 Hessian ``[term][pair][record]`` exactly as the reference lays them out
 (``autodiff.py:471-498``), so every warp store is a coalesced 256-byte run.
+
+:class:`HostLayout` is pure host work (no GPU) so that ``build()`` can
+pre-compile the exact module a model will use; :class:`DevicePlan` uploads it.
 """
 
 from __future__ import annotations
@@ -31,6 +34,12 @@ ALIGN = 32  # elements: 256 B for fp64, 128 B for int32
 
 KIND = {"objective": 0, "constraint": 1, "augment": 2}
 OP_LEAF, OP_ADD, OP_CONST, OP_ZERO_PLUS, OP_TOTAL_ADD = range(5)
+SEG_TERM, SEG_ROW, SEG_FOLD = 0, 1, 2
+
+# Models with at most this many terms get a *specialised* module (metadata
+# compiled in as constants); larger ones (e.g. thousands of per-instance
+# blocks) use the generic module with run-time term tables.
+META_CONST_MAX_TERMS = 80
 
 
 class _Blob:
@@ -110,135 +119,169 @@ def collect_patterns(plan):
     return pcodes, term_pid
 
 
-def precompile(plan) -> bytes:
-    """JIT (or fetch from cache) the module for a host plan; no GPU needed."""
-    pcodes, _ = collect_patterns(plan)
-    return compile_module(module_source(pcodes))
+def _row_layout(base_tp, base_dev, augs, dev_index):
+    """Contributions per base row in reference order (base, then augments in
+    registration order, records in order).  Returns ``(None, None, slots)`` for
+    the warp-fold layout -- rows packed into 32-lane warps, slot =
+    (term | position << 16, record), pad = (-1, 0) -- or ``(ptr, ent, None)``
+    for the serial CSR layout when a row has more than 32 contributions."""
+    n = base_tp.nrec
+    lrows, terms_, recs = [], [], []
+    for a in augs:
+        lrows.append(np.asarray(a.rows, dtype=np.int64) - base_tp.row_offset)
+        terms_.append(np.full(a.nrec, dev_index[id(a)], dtype=np.int64))
+        recs.append(np.arange(a.nrec, dtype=np.int64))
+    lrows = np.concatenate(lrows) if lrows else np.zeros(0, np.int64)
+    terms_ = np.concatenate(terms_) if terms_ else np.zeros(0, np.int64)
+    recs = np.concatenate(recs) if recs else np.zeros(0, np.int64)
+    order = np.argsort(lrows, kind="stable")
+    counts = np.bincount(lrows, minlength=n)
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=ptr[1:])
+    ent = np.stack([terms_[order], recs[order]], axis=1)
+    if (counts.size and counts.max() + 1 > 32) or len(dev_index) >= 2**16:
+        return _i32(ptr, "row CSR"), _i32(ent, "row CSR entries"), None
+    # greedy packing of rows (1 + augments each) into 32-lane warps
+    length = (counts + 1).astype(np.int64)
+    warp_of = np.zeros(n, dtype=np.int64)
+    lane0 = np.zeros(n, dtype=np.int64)
+    w, fill = 0, 0
+    for r, L in enumerate(length.tolist()):
+        if fill + L > 32:
+            w += 1
+            fill = 0
+        warp_of[r] = w
+        lane0[r] = fill
+        fill += L
+    n_warps = w + 1 if n else 0
+    slots = np.zeros((n_warps * 32, 2), dtype=np.int64)
+    slots[:, 0] = -1
+    base_slot = warp_of * 32 + lane0
+    slots[base_slot, 0] = base_dev
+    slots[base_slot, 1] = np.arange(n)
+    if ent.shape[0]:
+        row_of = lrows[order]
+        pos = np.arange(ent.shape[0]) - ptr[row_of] + 1  # 1-based position within the row
+        at = base_slot[row_of] + pos
+        slots[at, 0] = ent[:, 0] | (pos << 16)
+        slots[at, 1] = ent[:, 1]
+    return None, None, _i32(slots, "fold slots")
 
 
-class DevicePlan:
-    """The model's plan resident on one GPU, with its compiled kernels."""
+class HostLayout:
+    """Everything the device needs for one plan, built on the host only."""
 
-    def __init__(self, model, device=None):
-        import torch
-
-        if not torch.cuda.is_available():
-            raise _lib.ExaError("no CUDA device: the callback engine runs on B200 only (no CPU path)")
-        self.device = torch.cuda.current_device() if device is None else int(device)
-        plan = model.plan
-        self.model = model
+    def __init__(self, plan):
         self.plan = plan
+        self.threads = THREADS
         terms = plan.obj_terms + plan.con_terms
         self.terms = terms
         n_obj = len(plan.obj_terms)
         self.n_obj = n_obj
+        self.patterns, self.term_pid = collect_patterns(plan)
+        self.has_checks = any(pc.has_checks for pc in self.patterns)
+        pcs = self.patterns
 
-        # ---- patterns ---------------------------------------------------
-        pcodes, term_pid = collect_patterns(plan)
-        self.patterns = pcodes
-        self.term_pid = term_pid
-        self.has_checks = any(pc.has_checks for pc in pcodes)
-
-        # ---- augment CSR per target block -------------------------------
         dev_index = {id(tp): t for t, tp in enumerate(terms)}
         targets: dict = {}
         for tp in plan.con_terms:
             if tp.kind == "augment":
                 targets.setdefault(tp.target_index, []).append(tp)
-        base_of = {tp.block_index: tp for tp in plan.con_terms if tp.kind == "constraint"}
+        self._members: dict = {}
 
         f64 = _Blob(np.float64)
         i32 = _Blob(np.int32)
-        descs = (_lib.TermDesc * max(1, len(terms)))()
+        descs = []
+        self.fold_slots: dict = {}
         scr = 0
         self.scr0 = []
         for t, tp in enumerate(terms):
-            d = descs[t]
-            for i in range(_lib.MAXF):
-                d.f_off[i] = -1
-            for i in range(_lib.MAXI):
-                d.ix_off[i] = -1
-            for fi, name in enumerate(tp.tape.field_names):
-                d.f_off[fi] = f64.add(tp.reals[name])
-            for ii, name in enumerate(tp.tape.index_names):
-                d.ix_off[ii] = i32.add(_i32(tp.table.indices[name], f"index column {name!r}"))
-            for s, blk in enumerate(tp.slot_blocks):
-                d.voff[s] = blk.offset
-            d.rows_off = i32.add(_i32(tp.rows, "augment rows")) if tp.kind == "augment" else -1
-            d.row_ptr_off = -1
-            d.row_ent_off = -1
-            d.nrec = tp.nrec
-            d.pattern = term_pid[t]
-            d.kind = KIND[tp.kind]
-            d.order = t if tp.kind == "objective" else t - n_obj
-            d.row_offset = tp.row_offset if tp.row_offset is not None else 0
-            d.cons_direct = int(tp.kind == "constraint" and tp.block_index not in targets)
-            d.k = tp.tape.k
-            d.jac0 = tp.jac_slices[0][0] if (tp.kind != "objective" and tp.tape.k) else 0
-            d.hess0 = tp.hess_start
-            d.scr0 = scr if tp.kind == "objective" else 0
-            self.scr0.append(scr if tp.kind == "objective" else 0)
+            d = {
+                "f_off": [f64.add(tp.reals[nm]) for nm in tp.tape.field_names],
+                "ix_off": [i32.add(_i32(tp.table.indices[nm], f"index column {nm!r}"))
+                           for nm in tp.tape.index_names],
+                "voff": [blk.offset for blk in tp.slot_blocks],
+                "rows_off": i32.add(_i32(tp.rows, "augment rows")) if tp.kind == "augment" else -1,
+                "row_ptr_off": -1, "row_ent_off": -1,
+                "nrec": tp.nrec, "pattern": self.term_pid[t], "kind": KIND[tp.kind],
+                "order": t if tp.kind == "objective" else t - n_obj,
+                "row_offset": tp.row_offset if tp.row_offset is not None else 0,
+                "cons_direct": int(tp.kind == "constraint" and tp.block_index not in targets),
+                "k": tp.tape.k,
+                "jac0": tp.jac_slices[0][0] if (tp.kind != "objective" and tp.tape.k) else 0,
+                "hess0": tp.hess_start,
+                "scr0": scr if tp.kind == "objective" else 0,
+            }
+            self.scr0.append(d["scr0"])
             if tp.kind == "objective":
                 scr += max(tp.tape.k, 1) * tp.nrec
             if tp.kind == "constraint" and tp.block_index in targets:
-                ptr, ent = self._row_csr(tp, targets[tp.block_index], dev_index)
-                d.row_ptr_off = i32.add(ptr)
-                # int2 entries need 8-byte alignment: ALIGN keeps offsets even
-                d.row_ent_off = i32.add(ent)
+                augs = targets[tp.block_index]
+                self._members[t] = [t] + [dev_index[id(a)] for a in augs]
+                ptr, ent, slots = _row_layout(tp, t, augs, dev_index)
+                if slots is not None:  # int2 entries: ALIGN keeps offsets 8-byte aligned
+                    d["row_ent_off"] = i32.add(slots)
+                    self.fold_slots[t] = slots.shape[0]
+                else:
+                    d["row_ptr_off"] = i32.add(ptr)
+                    d["row_ent_off"] = i32.add(ent)
+            descs.append(d)
+        self.descs = descs
         self.n_scr = scr
-        del base_of
+        self.f64 = f64.array()
+        self.i32 = i32.array()
 
-        # ---- segments per callback ---------------------------------------
-        con = plan.con_terms
+        # ---- segments per callback -----------------------------------------
         segs = {m: [] for m in range(_lib.NMODES)}
 
         def seg(m, t, kind, nrec):
             if nrec > 0:
                 segs[m].append((t, kind, nrec))
 
-        pcs = pcodes
         for t, tp in enumerate(terms):
             k = tp.tape.k
-            chk = pcs[term_pid[t]].has_checks
+            chk = pcs[self.term_pid[t]].has_checks
             if tp.kind == "objective":
                 if k:
-                    seg(_lib.MODE_SET, t, 0, tp.nrec)
-                    seg(_lib.MODE_HESS, t, 0, tp.nrec)
+                    seg(_lib.MODE_SET, t, SEG_TERM, tp.nrec)
+                    seg(_lib.MODE_HESS, t, SEG_TERM, tp.nrec)
                 if k or chk:
-                    seg(_lib.MODE_GRAD, t, 0, tp.nrec)
-                if pcs[term_pid[t]].root_const is None or chk:
-                    seg(_lib.MODE_OBJV, t, 0, tp.nrec)
+                    seg(_lib.MODE_GRAD, t, SEG_TERM, tp.nrec)
+                if pcs[self.term_pid[t]].root_const is None or chk:
+                    seg(_lib.MODE_OBJV, t, SEG_TERM, tp.nrec)
                 continue
-            direct = bool(descs[t].cons_direct)
+            direct = bool(descs[t]["cons_direct"])
             if k or direct:
-                seg(_lib.MODE_SET, t, 0, tp.nrec)
+                seg(_lib.MODE_SET, t, SEG_TERM, tp.nrec)
             if direct:
-                seg(_lib.MODE_CONS, t, 0, tp.nrec)
+                seg(_lib.MODE_CONS, t, SEG_TERM, tp.nrec)
             if k or chk:
-                seg(_lib.MODE_JAC, t, 0, tp.nrec)
+                seg(_lib.MODE_JAC, t, SEG_TERM, tp.nrec)
             if k:
-                seg(_lib.MODE_HESS, t, 0, tp.nrec)
+                seg(_lib.MODE_HESS, t, SEG_TERM, tp.nrec)
             if tp.kind == "constraint" and not direct:
-                seg(_lib.MODE_SET, t, 1, tp.nrec)
-                seg(_lib.MODE_CONS, t, 1, tp.nrec)
-        self.segs = segs
-        seg_arrays = []
-        n_ctas = []
+                if t in self.fold_slots:
+                    seg(_lib.MODE_SET, t, SEG_FOLD, self.fold_slots[t])
+                    seg(_lib.MODE_CONS, t, SEG_FOLD, self.fold_slots[t])
+                else:
+                    seg(_lib.MODE_SET, t, SEG_ROW, tp.nrec)
+                    seg(_lib.MODE_CONS, t, SEG_ROW, tp.nrec)
+        self.segs = {}
+        self.n_ctas = []
         for m in range(_lib.NMODES):
-            arr = (_lib.SegDesc * max(1, len(segs[m])))()
             cta = 0
-            for s, (t, kind, nrec) in enumerate(segs[m]):
-                arr[s].term, arr[s].kind, arr[s].cta0, arr[s].nrec = t, kind, cta, nrec
+            lst = []
+            for (t, kind, nrec) in segs[m]:
+                lst.append((t, kind, cta, nrec))
                 cta += (nrec + THREADS - 1) // THREADS
-            seg_arrays.append(arr)
-            n_ctas.append(cta)
-        self.n_ctas = n_ctas
+            self.segs[m] = lst
+            self.n_ctas.append(cta)
 
-        # ---- objective program -----------------------------------------
+        # ---- objective program ---------------------------------------------
         leaves: list = []
         prog: list = []
         for t, tp in enumerate(plan.obj_terms):
-            rc = pcs[term_pid[t]].root_const
+            rc = pcs[self.term_pid[t]].root_const
             if rc is not None:
                 prog.append(_const_op(float(rc) * tp.nrec))
             elif tp.nrec == 0:
@@ -248,80 +291,24 @@ class DevicePlan:
                 pairwise_program(tp.nrec, self.scr0[t], leaves, prog)
                 prog.append((OP_ZERO_PLUS, 0, 0))
             prog.append((OP_TOTAL_ADD, 0, 0))
-        leaves_a = np.array(leaves, dtype=np.int64).reshape(-1, 2)
-        prog_a = np.array(prog, dtype=np.int64).reshape(-1, 3)
+        self.leaves = np.array(leaves, dtype=np.int64).reshape(-1, 2)
+        self.prog = np.array(prog, dtype=np.int64).reshape(-1, 3)
+        self.grad_ptr, self.grad_ent = self._grad_csr(plan.nvar)
 
-        # ---- gradient CSR over variables ------------------------------
-        gptr, gent = self._grad_csr(model.nvar)
+        # ---- module source ---------------------------------------------------
+        self.specialised = len(terms) <= META_CONST_MAX_TERMS
+        self.source = module_source(self.patterns, meta_const=False,
+                                    layout=self if self.specialised else None)
 
-        # ---- JIT ----------------------------------------------------------
-        self.source = module_source(pcodes)
-        self.cubin = compile_module(self.source)
+    # accessors used by the specialised-kernel generator (jit.py)
+    def term_descs(self):
+        return self.descs
 
-        f64a, i32a = f64.array(), i32.array()
-        desc = _lib.PlanDesc()
-        desc.abi_version = _lib.ABI_VERSION
-        desc.device = self.device
-        desc.nvar, desc.ncon = model.nvar, model.ncon
-        desc.n_jac, desc.n_hess = plan.n_jac_slots, plan.n_hess_slots
-        desc.f64 = f64a.ctypes.data_as(C.POINTER(C.c_double))
-        desc.n_f64 = f64a.size
-        desc.i32 = i32a.ctypes.data_as(C.POINTER(C.c_int32))
-        desc.n_i32 = i32a.size
-        desc.terms = C.cast(descs, C.POINTER(_lib.TermDesc))
-        desc.n_terms = len(terms)
-        desc.threads = THREADS
-        for m in range(_lib.NMODES):
-            desc.segs[m] = C.cast(seg_arrays[m], C.POINTER(_lib.SegDesc))
-            desc.n_segs[m] = len(segs[m])
-            desc.n_ctas[m] = n_ctas[m]
-        n_con_terms = len(con)
-        bases = {
-            _lib.MODE_SET: (n_con_terms, 0), _lib.MODE_CONS: (0, 0), _lib.MODE_JAC: (0, 0),
-            _lib.MODE_HESS: (0, n_obj), _lib.MODE_OBJV: (0, 0), _lib.MODE_GRAD: (0, 0),
-        }
-        for m, (ob, cb) in bases.items():
-            desc.err_base[m][0] = ob
-            desc.err_base[m][1] = cb
-        desc.n_vscr = desc.n_gscr = scr
-        desc.leaves = leaves_a.ctypes.data_as(C.POINTER(C.c_int64))
-        desc.n_leaves = leaves_a.shape[0]
-        desc.obj_prog = prog_a.ctypes.data_as(C.POINTER(C.c_int64))
-        desc.n_prog = prog_a.shape[0]
-        if gptr is not None:
-            desc.grad_ptr = gptr.ctypes.data_as(C.POINTER(C.c_int64))
-            desc.grad_ent = gent.ctypes.data_as(C.POINTER(C.c_int64))
-            desc.n_grad_ent = gent.size
-        cub = C.create_string_buffer(self.cubin, len(self.cubin))
-        desc.cubin = C.cast(cub, C.c_void_p)
-        desc.cubin_size = len(self.cubin)
-        desc.has_domain_checks = int(self.has_checks)
-        lib = _lib.load()
-        handle = C.c_void_p()
-        with torch.cuda.device(self.device):
-            _lib.check(lib.exa_plan_create(C.byref(desc), C.byref(handle)), "exa_plan_create")
-        self.handle = handle
-        self._lib = lib
-        self.device_bytes = int(f64a.nbytes + i32a.nbytes)
+    def row_members(self):
+        return self._members
 
-    # ------------------------------------------------------------------
-    @staticmethod
-    def _row_csr(base_tp, augs, dev_index):
-        """Entries (augment term, record) per base row, reference order."""
-        n = base_tp.nrec
-        lrows, terms_, recs = [], [], []
-        for a in augs:
-            lrows.append(np.asarray(a.rows, dtype=np.int64) - base_tp.row_offset)
-            terms_.append(np.full(a.nrec, dev_index[id(a)], dtype=np.int64))
-            recs.append(np.arange(a.nrec, dtype=np.int64))
-        lrows = np.concatenate(lrows) if lrows else np.zeros(0, np.int64)
-        terms_ = np.concatenate(terms_) if terms_ else np.zeros(0, np.int64)
-        recs = np.concatenate(recs) if recs else np.zeros(0, np.int64)
-        order = np.argsort(lrows, kind="stable")
-        ptr = np.zeros(n + 1, dtype=np.int64)
-        np.cumsum(np.bincount(lrows, minlength=n), out=ptr[1:])
-        ent = np.stack([terms_[order], recs[order]], axis=1)
-        return _i32(ptr, "row CSR"), _i32(ent, "row CSR entries")
+    def mode_segments(self, m):
+        return self.segs[m]
 
     def _grad_csr(self, nvar):
         plan = self.plan
@@ -347,10 +334,110 @@ class DevicePlan:
         np.cumsum(np.bincount(sv, minlength=nvar), out=ptr[1:])
         return ptr, ent
 
+
+def host_layout(plan) -> HostLayout:
+    lay = getattr(plan, "_exa_layout", None)
+    if lay is None or lay.threads != THREADS:
+        lay = HostLayout(plan)
+        plan._exa_layout = lay
+    return lay
+
+
+def precompile(plan) -> bytes:
+    """JIT (or fetch from cache) the module for a host plan; no GPU needed."""
+    return compile_module(host_layout(plan).source)
+
+
+class DevicePlan:
+    """The model's plan resident on one GPU, with its compiled kernels."""
+
+    def __init__(self, model, device=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise _lib.ExaError("no CUDA device: the callback engine runs on B200 only (no CPU path)")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        plan = model.plan
+        self.model = model
+        self.plan = plan
+        lay = host_layout(plan)
+        self.layout = lay
+        self.patterns = lay.patterns
+        self.has_checks = lay.has_checks
+        self.n_ctas = lay.n_ctas
+        self.cubin = compile_module(lay.source)
+
+        terms = lay.terms
+        descs = (_lib.TermDesc * max(1, len(terms)))()
+        for t, d in enumerate(lay.descs):
+            td = descs[t]
+            for i in range(_lib.MAXF):
+                td.f_off[i] = d["f_off"][i] if i < len(d["f_off"]) else -1
+            for i in range(_lib.MAXI):
+                td.ix_off[i] = d["ix_off"][i] if i < len(d["ix_off"]) else -1
+            for s, vo in enumerate(d["voff"]):
+                td.voff[s] = vo
+            for k in ("rows_off", "row_ptr_off", "row_ent_off", "nrec", "pattern", "kind", "order",
+                      "row_offset", "cons_direct", "k", "jac0", "hess0", "scr0"):
+                setattr(td, k, d[k])
+        seg_arrays = []
+        for m in range(_lib.NMODES):
+            lst = lay.segs[m]
+            arr = (_lib.SegDesc * max(1, len(lst)))()
+            for s, (t, kind, cta0, nrec) in enumerate(lst):
+                arr[s].term, arr[s].kind, arr[s].cta0, arr[s].nrec = t, kind, cta0, nrec
+            seg_arrays.append(arr)
+
+        desc = _lib.PlanDesc()
+        desc.abi_version = _lib.ABI_VERSION
+        desc.device = self.device
+        desc.nvar, desc.ncon = model.nvar, model.ncon
+        desc.n_jac, desc.n_hess = plan.n_jac_slots, plan.n_hess_slots
+        desc.f64 = lay.f64.ctypes.data_as(C.POINTER(C.c_double))
+        desc.n_f64 = lay.f64.size
+        desc.i32 = lay.i32.ctypes.data_as(C.POINTER(C.c_int32))
+        desc.n_i32 = lay.i32.size
+        desc.terms = C.cast(descs, C.POINTER(_lib.TermDesc))
+        desc.n_terms = len(terms)
+        desc.threads = lay.threads
+        for m in range(_lib.NMODES):
+            desc.segs[m] = C.cast(seg_arrays[m], C.POINTER(_lib.SegDesc))
+            desc.n_segs[m] = len(lay.segs[m])
+            desc.n_ctas[m] = lay.n_ctas[m]
+        n_obj, n_con = len(plan.obj_terms), len(plan.con_terms)
+        bases = {
+            _lib.MODE_SET: (n_con, 0), _lib.MODE_CONS: (0, 0), _lib.MODE_JAC: (0, 0),
+            _lib.MODE_HESS: (0, n_obj), _lib.MODE_OBJV: (0, 0), _lib.MODE_GRAD: (0, 0),
+        }
+        for m, (ob, cb) in bases.items():
+            desc.err_base[m][0] = ob
+            desc.err_base[m][1] = cb
+        desc.n_vscr = desc.n_gscr = lay.n_scr
+        desc.leaves = lay.leaves.ctypes.data_as(C.POINTER(C.c_int64))
+        desc.n_leaves = lay.leaves.shape[0]
+        desc.obj_prog = lay.prog.ctypes.data_as(C.POINTER(C.c_int64))
+        desc.n_prog = lay.prog.shape[0]
+        if lay.grad_ptr is not None:
+            desc.grad_ptr = lay.grad_ptr.ctypes.data_as(C.POINTER(C.c_int64))
+            desc.grad_ent = lay.grad_ent.ctypes.data_as(C.POINTER(C.c_int64))
+            desc.n_grad_ent = lay.grad_ent.size
+        cub = C.create_string_buffer(self.cubin, len(self.cubin))
+        desc.cubin = C.cast(cub, C.c_void_p)
+        desc.cubin_size = len(self.cubin)
+        desc.has_domain_checks = int(self.has_checks)
+        lib = _lib.load()
+        handle = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(lib.exa_plan_create(C.byref(desc), C.byref(handle)), "exa_plan_create")
+        self.handle = handle
+        self._lib = lib
+        self.device_bytes = int(lay.f64.nbytes + lay.i32.nbytes)
+
     def info(self):
         b, r = C.c_int64(), C.c_int32()
         _lib.check(self._lib.exa_plan_info(self.handle, C.byref(b), C.byref(r)), "plan_info")
         return {"device_bytes": b.value, "regs_set_kernel": r.value, "patterns": len(self.patterns),
+                "specialised": self.layout.specialised,
                 "ctas": dict(zip(("set", "cons", "jac", "hess", "objv", "grad"), self.n_ctas))}
 
     def __del__(self):
