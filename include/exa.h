@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define EXA_ABI_VERSION 1
+#define EXA_ABI_VERSION 2
 #define EXA_MAXF 16
 #define EXA_MAXI 16
 #define EXA_MAXK 16
@@ -52,6 +52,10 @@ extern "C" {
 #define EXA_MODE_OBJV 4
 #define EXA_MODE_GRAD 5
 #define EXA_NMODES 6
+/* each callback runs as up to two concurrent kernels: heavy patterns
+ * (transcendentals / many slots, small CTAs) and light ones (large CTAs, few
+ * registers); kernel id = 2 * mode + {0 heavy, 1 light} */
+#define EXA_NKERN 12
 
 typedef struct ExaPlan ExaPlan;
 typedef struct ExaWorkspace ExaWorkspace;
@@ -86,10 +90,10 @@ typedef struct ExaPlanDesc {
   int64_t n_i32;
   const ExaTermDesc* terms;
   int32_t n_terms;
-  int32_t threads; /* CTA size the module was generated for */
-  const ExaSegDesc* segs[EXA_NMODES];
-  int32_t n_segs[EXA_NMODES];
-  int32_t n_ctas[EXA_NMODES];
+  int32_t threads[2]; /* CTA size of the heavy / light kernels of the module */
+  const ExaSegDesc* segs[EXA_NKERN];
+  int32_t n_segs[EXA_NKERN];
+  int32_t n_ctas[EXA_NKERN];
   int32_t err_base[EXA_NMODES][2]; /* domain-error rank offsets: {objective, constraint} */
   /* objective: per-record value scratch, leaves and combine program
      (numpy pairwise summation order) */

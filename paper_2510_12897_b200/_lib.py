@@ -14,8 +14,9 @@ LIB_PATH = Path(os.environ.get("EXA_LIB", Path(__file__).resolve().parent / "lib
 
 MAXF = MAXI = MAXK = 16
 NMODES = 6
+NKERN = 12
 MODE_SET, MODE_CONS, MODE_JAC, MODE_HESS, MODE_OBJV, MODE_GRAD = range(6)
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 i64, i32, dbl, vp = C.c_int64, C.c_int32, C.c_double, C.c_void_p
 
@@ -39,8 +40,8 @@ class PlanDesc(C.Structure):
         ("nvar", i64), ("ncon", i64), ("n_jac", i64), ("n_hess", i64),
         ("f64", C.POINTER(dbl)), ("n_f64", i64),
         ("i32", C.POINTER(i32)), ("n_i32", i64),
-        ("terms", C.POINTER(TermDesc)), ("n_terms", i32), ("threads", i32),
-        ("segs", C.POINTER(SegDesc) * NMODES), ("n_segs", i32 * NMODES), ("n_ctas", i32 * NMODES),
+        ("terms", C.POINTER(TermDesc)), ("n_terms", i32), ("threads", i32 * 2),
+        ("segs", C.POINTER(SegDesc) * NKERN), ("n_segs", i32 * NKERN), ("n_ctas", i32 * NKERN),
         ("err_base", (i32 * 2) * NMODES),
         ("n_vscr", i64), ("n_gscr", i64),
         ("leaves", C.POINTER(i64)), ("n_leaves", i32),

@@ -32,6 +32,7 @@ Only exact rewrites are applied (x*1 -> x, x*-1 -> -x, x/1 -> x, x-(+0) -> x);
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -46,10 +47,26 @@ class Arr:
 
 
 class Sym:
-    __slots__ = ("name",)
+    """A data-dependent value held in a CUDA local.  ``nz`` records that the
+    value can never be -0.0 (then ``0.0 + x == x`` bitwise and the add is
+    dropped): true for ``0 + x``, for any sum/difference whose first operand
+    (or, for sums, either operand) can never be -0.0 -- IEEE round-to-nearest
+    gives -0.0 from a + b only for (-0) + (-0) and from a - b only for
+    (-0) - (+0) -- and for cos(), which is never zero for a double argument."""
 
-    def __init__(self, name: str):
+    __slots__ = ("name", "nz")
+
+    def __init__(self, name: str, nz: bool = False):
         self.name = name
+        self.nz = nz
+
+
+def _nz(v) -> bool:
+    """Value can never be -0.0."""
+    if isinstance(v, Sym):
+        return v.nz
+    c = v.value if isinstance(v, Arr) else float(v)
+    return not (c == 0.0 and math.copysign(1.0, c) < 0)
 
 
 def _is_zero(v) -> bool:
@@ -92,14 +109,14 @@ class Gen:
         self.sincos: dict = {}
         self.checks: list = []
 
-    def new(self, expr: str) -> Sym:
+    def new(self, expr: str, nz: bool = False) -> Sym:
         got = self.memo.get(expr)
         if got is not None:
             return got
         name = f"t{self.n}"
         self.n += 1
         self.lines.append(f"  const double {name} = {expr};")
-        s = Sym(name)
+        s = Sym(name, nz)
         self.memo[expr] = s
         return s
 
@@ -136,12 +153,14 @@ class Gen:
             if cb == 0.0 and not math.copysign(1.0, cb) < 0:
                 return a
         elif op == "add":
-            if cb == 0.0 and math.copysign(1.0, cb) < 0:
+            # x + (-0) == x;  (+0) + x == x unless x is -0.0
+            if cb == 0.0 and (math.copysign(1.0, cb) < 0 or _nz(a)):
                 return a
-            if ca == 0.0 and math.copysign(1.0, ca) < 0:
+            if ca == 0.0 and (math.copysign(1.0, ca) < 0 or _nz(b)):
                 return b
         sym = {"add": "+", "sub": "-", "mul": "*", "div": "/"}[op]
-        return self.new(f"{self.r(a)} {sym} {self.r(b)}")
+        nz = (op == "add" and (_nz(a) or _nz(b))) or (op == "sub" and _nz(a))
+        return self.new(f"{self.r(a)} {sym} {self.r(b)}", nz)
 
     def add(self, a, b):
         return self.bin("add", a, b)
@@ -174,7 +193,7 @@ class Gen:
             if pair is None:
                 s, c = f"s_{a.name}", f"c_{a.name}"
                 self.lines.append(f"  double {s}, {c}; exa_sincos({a.name}, &{s}, &{c});")
-                pair = (Sym(s), Sym(c))
+                pair = (Sym(s), Sym(c, nz=True))  # cos(x) != 0 for every double x
                 self.sincos[a.name] = pair
             return pair[0] if name == "sin" else pair[1]
         return self.new(f"{name}({a.name})")
@@ -490,6 +509,7 @@ class PatternCode:
             loads["field"][fname] = Sym(f"f{fi}")
         for ii in range(self.ni):
             pre.append(f"  const int i{ii} = __ldg(T.ix[{ii}] + r);")
+        pre_wait = len(pre)
         for s, (_, ic) in enumerate(self.slot_struct):
             pre.append(f"  const int c{s} = T.voff[{s}] + i{ic};")
             pre.append(f"  const double x{s} = __ldg(A.x + c{s});")
@@ -523,13 +543,24 @@ class PatternCode:
         out.append(f"  return {R(value_root)};")
         out.append("}")
 
-        # full term function, MODE-templated; unused temps are dead code
+        # full term function, MODE-templated; unused temps are dead code.  All
+        # loads (including the Hessian weight) are issued before the first
+        # store, and outputs are __restrict__, so several records per thread
+        # (light patterns) overlap their memory latency.
         out.append(f"template <int MODE>\n__device__ __forceinline__ void exa_term_{pid}(const ExaTerm& T, int r, const ExaArgs& A, int rank) {{")
-        out.extend(pre)
+        out.append("  double* __restrict__ Cout = A.c;")
+        out.append("  double* __restrict__ Jout = A.J;")
+        out.append("  double* __restrict__ Hout = A.H;")
+        out.extend(pre[:pre_wait])
+        out.append("  EXA_GRID_WAIT();")
+        out.extend(pre[pre_wait:])
+        if k:
+            out.append("  const double wgt = !(MODE & EXA_M_HESS) ? 0.0 : (T.kind == EXA_OBJ) ? A.w"
+                       " : __ldg(A.y + (T.rows ? __ldg(T.rows + r) : T.row_offset + r));")
         out.extend(value_lines)
         out.append("  if (MODE & (EXA_M_CONS | EXA_M_OBJV)) {")
         out.append(f"    const double root = {R(value_root)};")
-        out.append("    if ((MODE & EXA_M_CONS) && T.cons_direct) A.c[T.row_offset + r] = 0.0 + root;")
+        out.append("    if ((MODE & EXA_M_CONS) && T.cons_direct) Cout[T.row_offset + r] = 0.0 + root;")
         out.append("    if ((MODE & EXA_M_OBJV) && T.kind == EXA_OBJ) A.V[T.scr0 + r] = root;")
         out.append("  }")
         if k:
@@ -537,14 +568,13 @@ class PatternCode:
             out.extend("  " + l for l in body_grad)
             out.append("    if ((MODE & EXA_M_JAC) && T.kind != EXA_OBJ) {")
             for s in range(k):
-                out.append(f"      A.J[T.jac0 + {s}LL * T.nrec + r] = {R(grads[s])};")
+                out.append(f"      Jout[T.jac0 + {s}LL * T.nrec + r] = {R(grads[s])};")
             out.append("    }")
             out.append("    if ((MODE & EXA_M_GRAD) && T.kind == EXA_OBJ) {")
             for s in range(k):
                 out.append(f"      A.G[T.scr0 + {s}LL * T.nrec + r] = {R(grads[s])};")
             out.append("    }")
             out.append("    if (MODE & EXA_M_HESS) {")
-            out.append("      const double wgt = (T.kind == EXA_OBJ) ? A.w : __ldg(A.y + (T.rows ? __ldg(T.rows + r) : T.row_offset + r));")
             out.extend("    " + l for l in body_hess)
             pair = 0
             for i in range(k):
@@ -554,11 +584,17 @@ class PatternCode:
                     bi, bj = self.slot_struct[i][0], self.slot_struct[j][0]
                     if i != j and bi == bj:
                         expr = f"(c{i} == c{j} ? {expr} * 2.0 : {expr})"
-                    out.append(f"      A.H[T.hess0 + {pair}LL * T.nrec + r] = wgt * {expr};")
+                    out.append(f"      Hout[T.hess0 + {pair}LL * T.nrec + r] = wgt * {expr};")
                     pair += 1
             out.append("    }")
             out.append("  }")
         out.append("}")
+        # records per thread: light patterns amortise per-thread overheads and
+        # overlap several records' loads; heavy ones keep one record per thread
+        n_ops = len(g.lines)
+        heavy = bool(g.sincos) or any(ins[0] in ("exp", "log", "pow") for ins in self.instr) or k > 2
+        self.rpt = int(os.environ.get("EXA_RPT_LIGHT", "1")) if (not heavy and n_ops <= 40) else 1
+        self.heavy = heavy
         return "\n".join(out)
 
     def tape_norm(self):

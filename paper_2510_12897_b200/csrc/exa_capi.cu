@@ -56,8 +56,9 @@ int dev_upload(T** dst, const T* src, size_t n) {
   return 0;
 }
 
-const char* kKernelNames[EXA_NMODES] = {"exa_k_set", "exa_k_cons", "exa_k_jac",
-                                        "exa_k_hess", "exa_k_objv", "exa_k_grad"};
+const char* kKernelNames[EXA_NKERN] = {
+    "exa_k_set_h",  "exa_k_set_l",  "exa_k_cons_h", "exa_k_cons_l", "exa_k_jac_h",  "exa_k_jac_l",
+    "exa_k_hess_h", "exa_k_hess_l", "exa_k_objv_h", "exa_k_objv_l", "exa_k_grad_h", "exa_k_grad_l"};
 
 // objective combine program opcodes (see paper_2510_12897_b200/device.py)
 enum { OP_LEAF = 0, OP_ADD = 1, OP_CONST = 2, OP_ZERO_PLUS = 3, OP_TOTAL_ADD = 4 };
@@ -70,20 +71,22 @@ struct ExaWorkspace {
   double* G = nullptr;
   double* leafsum = nullptr;
   unsigned long long* err = nullptr;
+  cudaStream_t aux = nullptr;   // second stream: light kernel runs beside the heavy one
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 struct ExaPlan {
   int device = 0;
   int64_t nvar = 0, ncon = 0, n_jac = 0, n_hess = 0;
-  int threads = 256;
+  int threads[2] = {128, 256};
   double* f64 = nullptr;
   int32_t* i32 = nullptr;
   ExaTerm* terms = nullptr;
   int32_t n_terms = 0;
-  ExaSeg* segs[EXA_NMODES] = {};
-  int* cta_seg[EXA_NMODES] = {};
-  int n_ctas[EXA_NMODES] = {};
-  int n_segs_mode[EXA_NMODES] = {};
+  ExaSeg* segs[EXA_NKERN] = {};
+  int* cta_seg[EXA_NKERN] = {};
+  int n_ctas[EXA_NKERN] = {};
+  int n_segs_mode[EXA_NKERN] = {};
   int err_base[EXA_NMODES][2] = {};
   int64_t n_vscr = 0, n_gscr = 0;
   int64_t* leaves = nullptr;
@@ -94,10 +97,11 @@ struct ExaPlan {
   int64_t* grad_ent = nullptr;
   int has_checks = 0;
   cudaLibrary_t lib = nullptr;
-  cudaKernel_t kern[EXA_NMODES] = {};
+  cudaKernel_t kern[EXA_NKERN] = {};
   ExaWorkspace* dflt = nullptr;
   size_t bytes = 0;
-  int seg_off[EXA_NMODES] = {};
+  int pdl = 0;
+  int seg_off[EXA_NKERN] = {};
   bool meta_const = false;
 };
 
@@ -265,6 +269,9 @@ static int ws_alloc(ExaPlan* p, ExaWorkspace** out) {
   if (p->n_leaves) CU(cudaMalloc((void**)&w->leafsum, p->n_leaves * sizeof(double)));
   CU(cudaMalloc((void**)&w->err, sizeof(unsigned long long)));
   CU(cudaMemset(w->err, 0xff, sizeof(unsigned long long)));
+  CU(cudaStreamCreateWithFlags(&w->aux, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&w->join, cudaEventDisableTiming));
   *out = w;
   return 0;
 }
@@ -275,6 +282,9 @@ void exa_workspace_destroy(ExaWorkspace* w) {
   cudaFree(w->G);
   cudaFree(w->leafsum);
   cudaFree(w->err);
+  if (w->fork) cudaEventDestroy(w->fork);
+  if (w->join) cudaEventDestroy(w->join);
+  if (w->aux) cudaStreamDestroy(w->aux);
   delete w;
 }
 
@@ -291,7 +301,7 @@ void exa_plan_destroy(ExaPlan* p) {
   cudaFree(p->f64);
   cudaFree(p->i32);
   cudaFree(p->terms);
-  for (int m = 0; m < EXA_NMODES; ++m) {
+  for (int m = 0; m < EXA_NKERN; ++m) {
     cudaFree(p->segs[m]);
     cudaFree(p->cta_seg[m]);
   }
@@ -320,7 +330,12 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
   p->ncon = d->ncon;
   p->n_jac = d->n_jac;
   p->n_hess = d->n_hess;
-  p->threads = d->threads > 0 ? d->threads : 256;
+  {
+    const char* e = getenv("EXA_PDL");  // programmatic dependent launch: opt-in (no measured gain)
+    p->pdl = (e && e[0] == '1') ? 1 : 0;
+  }
+  p->threads[0] = d->threads[0] > 0 ? d->threads[0] : 128;
+  p->threads[1] = d->threads[1] > 0 ? d->threads[1] : 256;
   p->n_terms = d->n_terms;
   p->has_checks = d->has_domain_checks;
   p->n_vscr = d->n_vscr;
@@ -357,25 +372,29 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
   p->bytes += terms.size() * sizeof(ExaTerm);
 
   for (int m = 0; m < EXA_NMODES; ++m) {
-    const int ns = d->n_segs[m];
-    p->n_segs_mode[m] = ns;
-    p->n_ctas[m] = d->n_ctas[m];
     p->err_base[m][0] = d->err_base[m][0];
     p->err_base[m][1] = d->err_base[m][1];
+  }
+  for (int kid = 0; kid < EXA_NKERN; ++kid) {
+    const int ns = d->n_segs[kid];
+    const int th = p->threads[kid & 1];
+    p->n_segs_mode[kid] = ns;
+    p->n_ctas[kid] = d->n_ctas[kid];
     if (ns == 0) continue;
-    if ((rc = dev_upload(&p->segs[m], reinterpret_cast<const ExaSeg*>(d->segs[m]), (size_t)ns))) return bail(rc);
-    std::vector<int> map(d->n_ctas[m], -1);
+    if ((rc = dev_upload(&p->segs[kid], reinterpret_cast<const ExaSeg*>(d->segs[kid]), (size_t)ns))) return bail(rc);
+    std::vector<int> map(d->n_ctas[kid], -1);
     for (int s = 0; s < ns; ++s) {
-      const ExaSegDesc& sg = d->segs[m][s];
-      const int nc = (sg.nrec + p->threads - 1) / p->threads;
+      const ExaSegDesc& sg = d->segs[kid][s];
+      const int rpt = (sg.kind >> 8) > 0 ? (sg.kind >> 8) : 1;  // records per thread
+      const int nc = (sg.nrec + th * rpt - 1) / (th * rpt);
       for (int c = 0; c < nc; ++c) {
-        if (sg.cta0 + c >= d->n_ctas[m]) return bail(fail("mode %d: segment %d overflows the grid", m, s));
+        if (sg.cta0 + c >= d->n_ctas[kid]) return bail(fail("kernel %d: segment %d overflows the grid", kid, s));
         map[sg.cta0 + c] = s;
       }
     }
-    for (int c = 0; c < d->n_ctas[m]; ++c)
-      if (map[c] < 0) return bail(fail("mode %d: CTA %d has no segment", m, c));
-    if ((rc = dev_upload(&p->cta_seg[m], map.data(), map.size()))) return bail(rc);
+    for (int c = 0; c < d->n_ctas[kid]; ++c)
+      if (map[c] < 0) return bail(fail("kernel %d: CTA %d has no segment", kid, c));
+    if ((rc = dev_upload(&p->cta_seg[kid], map.data(), map.size()))) return bail(rc);
     p->bytes += ns * sizeof(ExaSeg) + map.size() * sizeof(int);
   }
 
@@ -390,9 +409,10 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
 
   cudaError_t e = cudaLibraryLoadData(&p->lib, d->cubin, nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e != cudaSuccess) return bail(fail("cudaLibraryLoadData: %s", cudaGetErrorString(e)));
-  for (int m = 0; m < EXA_NMODES; ++m) {
-    e = cudaLibraryGetKernel(&p->kern[m], p->lib, kKernelNames[m]);
-    if (e != cudaSuccess) return bail(fail("cudaLibraryGetKernel(%s): %s", kKernelNames[m], cudaGetErrorString(e)));
+  for (int kid = 0; kid < EXA_NKERN; ++kid) {
+    e = cudaLibraryGetKernel(&p->kern[kid], p->lib, kKernelNames[kid]);
+    if (e != cudaSuccess)
+      return bail(fail("cudaLibraryGetKernel(%s): %s", kKernelNames[kid], cudaGetErrorString(e)));
   }
   // Constant-memory metadata variant: the module declares exa_terms_c /
   // exa_segs_c; fill them with the term table and all callbacks' segments.
@@ -403,9 +423,9 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
     if (cudaLibraryGetGlobal(&cterms, &nb_t, p->lib, "exa_terms_c") == cudaSuccess &&
         cudaLibraryGetGlobal(&csegs, &nb_s, p->lib, "exa_segs_c") == cudaSuccess) {
       std::vector<ExaSeg> all;
-      for (int m = 0; m < EXA_NMODES; ++m) {
-        p->seg_off[m] = (int)all.size();
-        for (int s = 0; s < d->n_segs[m]; ++s) all.push_back(reinterpret_cast<const ExaSeg*>(d->segs[m])[s]);
+      for (int kid = 0; kid < EXA_NKERN; ++kid) {
+        p->seg_off[kid] = (int)all.size();
+        for (int s = 0; s < d->n_segs[kid]; ++s) all.push_back(reinterpret_cast<const ExaSeg*>(d->segs[kid])[s]);
       }
       if (terms.size() * sizeof(ExaTerm) > nb_t || all.size() * sizeof(ExaSeg) > nb_s)
         return bail(fail("model too large for the constant-metadata module variant"));
@@ -432,22 +452,54 @@ int exa_plan_info(const ExaPlan* p, int64_t* bytes, int32_t* regs) {
   return 0;
 }
 
+static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStream_t st) {
+  A.seg_off = p->seg_off[kid];
+  A.n_segs = p->n_segs_mode[kid];
+  const ExaTerm* terms = p->terms;
+  const ExaSeg* segs = p->segs[kid];
+  const int* cmap = p->cta_seg[kid];
+  void* args[] = {(void*)&terms, (void*)&segs, (void*)&cmap, (void*)&A};
+  // Programmatic dependent launch: this kernel may be scheduled while the
+  // previous work on the stream drains; it loads the (immutable) plan data,
+  // then waits (griddepcontrol.wait) before touching caller buffers.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p->n_ctas[kid]);
+  cfg.blockDim = dim3(p->threads[kid & 1]);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = p->pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CU(cudaLaunchKernelExC(&cfg, (const void*)p->kern[kid], args));
+  return 0;
+}
+
+// One callback = its heavy kernel on `st` and its light kernel on the
+// workspace's aux stream, forked/joined with events (graph-capturable).
 static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaStream_t st) {
-  if (p->n_ctas[mode] == 0) return 0;
   A.err = w->err;
   A.obj_base = p->err_base[mode][0];
   A.con_base = p->err_base[mode][1];
-  A.seg_off = p->seg_off[mode];
   A.f64 = p->f64;
   A.i32 = p->i32;
-  A.n_segs = 0;
-  A.n_segs = p->n_segs_mode[mode];
-  const ExaTerm* terms = p->terms;
-  const ExaSeg* segs = p->segs[mode];
-  const int* cmap = p->cta_seg[mode];
-  void* args[] = {(void*)&terms, (void*)&segs, (void*)&cmap, (void*)&A};
-  CU(cudaLaunchKernel((const void*)p->kern[mode], dim3(p->n_ctas[mode]), dim3(p->threads), args, 0, st));
-  return 0;
+  const int kh = 2 * mode, kl = 2 * mode + 1;
+  const bool h = p->n_ctas[kh] > 0, l = p->n_ctas[kl] > 0;
+  int rc = 0;
+  if (h && l) {
+    CU(cudaEventRecord(w->fork, st));
+    CU(cudaStreamWaitEvent(w->aux, w->fork, 0));
+    if ((rc = launch_kid(p, w, kl, A, w->aux))) return rc;
+    if ((rc = launch_kid(p, w, kh, A, st))) return rc;
+    CU(cudaEventRecord(w->join, w->aux));
+    CU(cudaStreamWaitEvent(st, w->join, 0));
+  } else if (h) {
+    rc = launch_kid(p, w, kh, A, st);
+  } else if (l) {
+    rc = launch_kid(p, w, kl, A, st);
+  }
+  return rc;
 }
 
 static int reset_err(ExaPlan* p, ExaWorkspace* w, cudaStream_t st) {

@@ -120,6 +120,83 @@ EXA_FN void exa_sincos_reduced(exa_dd r, exa_dd* s_out, exa_dd* c_out) {
   *c_out = cr;
 }
 
+/* Half an ulp of |v| (v normal, finite). */
+EXA_FN double exa_half_ulp(double v) {
+#if defined(__CUDACC_RTC__) || defined(__CUDACC__)
+  long long b = __double_as_longlong(v) & 0x7ff0000000000000LL;
+  return __longlong_as_double(b) * 0x1p-53;
+#else
+  union { double d; long long i; } u;
+  u.d = v;
+  u.i &= 0x7ff0000000000000LL;
+  return u.d * 0x1p-53;
+#endif
+}
+
+EXA_FN int exa_mant_zero(double v) {
+#if defined(__CUDACC_RTC__) || defined(__CUDACC__)
+  return (__double_as_longlong(v) & 0x000fffffffffffffLL) == 0;
+#else
+  union { double d; long long i; } u;
+  u.d = v;
+  return (u.i & 0x000fffffffffffffLL) == 0;
+#endif
+}
+
+/* Round h + t (|t| << |h|) to nearest when the exact value is known to lie
+ * within err of h + t; returns 0 when the rounding cannot be decided. */
+EXA_FN int exa_round_decided(double h, double t, double err, double* out) {
+  exa_dd n = exa_fast_two_sum(h, t);
+  if (exa_mant_zero(n.hi)) return 0; /* binade edge: let the slow path decide */
+  if (fabs(n.lo) + err < exa_half_ulp(n.hi)) {
+    *out = n.hi;
+    return 1;
+  }
+  return 0;
+}
+
+/* Fast path for |x| <= pi/4: plain double evaluation with a running error
+ * bound; the result is returned only when that bound proves it is the
+ * correctly rounded value (Ziv's strategy).  Otherwise 0 -> slow path. */
+EXA_FN int exa_sincos_fast(double ax, double* s_out, double* c_out) {
+  const double jd = rint(ax * 64.0);
+  const double d = ax - jd * 0.015625; /* exact */
+  const double z = d * d;
+  /* sin d = d + d*ps,  ps = z*(-1/6 + z/120 - z^2/5040 + z^3/362880) */
+  const double ps = z * fma(z, fma(z, fma(z, 0x1.71de3a556c734p-19, -0x1.a01a01a01a01ap-13), 0x1.1111111111111p-7),
+                            -0x1.5555555555555p-3);
+  /* cos d - 1 = z*(-1/2 + z/24 - z^2/720 + z^3/40320 - z^4/3628800) */
+  const double cm1 = z * fma(z, fma(z, fma(z, fma(z, -0x1.27e4fb7789f5cp-22, 0x1.a01a01a01a01ap-16),
+                                               -0x1.6c16c16c16c17p-10), 0x1.5555555555555p-5), -0.5);
+  const double sdl = d * ps;
+  const int j = (int)jd;
+  double sv, cv;
+  if (j == 0) {
+    if (!exa_round_decided(d, sdl, 0x1p-49 * fabs(sdl), &sv)) return 0;
+    if (!exa_round_decided(1.0, cm1, 0x1p-49 * fabs(cm1), &cv)) return 0;
+  } else {
+    const double S0h = exa_sc_tab[j][0], S0l = exa_sc_tab[j][1];
+    const double C0h = exa_sc_tab[j][2], C0l = exa_sc_tab[j][3];
+    /* sin x = S0 + C0 d + (S0 cm1 + C0 d ps) */
+    exa_dd p = exa_two_prod(C0h, d);
+    exa_dd h = exa_two_sum(S0h, p.hi);
+    const double a1 = S0h * cm1, a2 = C0h * sdl;
+    double t = h.lo + (p.lo + (S0l + (C0l * d + (a1 + a2))));
+    double err = 0x1p-49 * (fabs(a1) + fabs(a2)) + 0x1p-96 * fabs(h.hi);
+    if (!exa_round_decided(h.hi, t, err, &sv)) return 0;
+    /* cos x = C0 - S0 d + (C0 cm1 - S0 d ps) */
+    exa_dd q = exa_two_prod(S0h, d);
+    exa_dd g = exa_two_sum(C0h, -q.hi);
+    const double b1 = C0h * cm1, b2 = S0h * sdl;
+    t = g.lo + (-q.lo + (C0l + (-(S0l * d) + (b1 - b2))));
+    err = 0x1p-49 * (fabs(b1) + fabs(b2)) + 0x1p-96 * fabs(g.hi);
+    if (!exa_round_decided(g.hi, t, err, &cv)) return 0;
+  }
+  *s_out = sv;
+  *c_out = cv;
+  return 1;
+}
+
 /* Correctly rounded (barring hard cases) sin and cos of x. */
 EXA_FN void exa_sincos(double x, double* s_out, double* c_out) {
   double ax = fabs(x);
@@ -132,6 +209,14 @@ EXA_FN void exa_sincos(double x, double* s_out, double* c_out) {
     *s_out = x;
     *c_out = 1.0;
     return;
+  }
+  if (ax <= EXA_PIO4) {
+    double sf, cf;
+    if (exa_sincos_fast(ax, &sf, &cf)) {
+      *s_out = x < 0.0 ? -sf : sf;
+      *c_out = cf;
+      return;
+    }
   }
   exa_dd r;
   int q = 0;

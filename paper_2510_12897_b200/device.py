@@ -22,13 +22,14 @@ pre-compile the exact module a model will use; :class:`DevicePlan` uploads it.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
 from . import _lib
 from .codegen import PatternCode
 from .core import ModelError
-from .jit import THREADS, compile_module, module_source
+from .jit import THREADS, THREADS_HEAVY, compile_module, module_source
 
 ALIGN = 32  # elements: 256 B for fp64, 128 B for int32
 
@@ -40,6 +41,10 @@ SEG_TERM, SEG_ROW, SEG_FOLD = 0, 1, 2
 # compiled in as constants); larger ones (e.g. thousands of per-instance
 # blocks) use the generic module with run-time term tables.
 META_CONST_MAX_TERMS = 80
+
+# Run heavy patterns in a separate concurrent kernel (measured slower on
+# case13659: the fork/join costs more than the register specialisation wins).
+SPLIT_HEAVY = os.environ.get("EXA_SPLIT", "0") == "1"
 
 
 class _Blob:
@@ -173,7 +178,7 @@ class HostLayout:
 
     def __init__(self, plan):
         self.plan = plan
-        self.threads = THREADS
+        self.threads = (THREADS_HEAVY, THREADS)
         terms = plan.obj_terms + plan.con_terms
         self.terms = terms
         n_obj = len(plan.obj_terms)
@@ -266,16 +271,33 @@ class HostLayout:
                 else:
                     seg(_lib.MODE_SET, t, SEG_ROW, tp.nrec)
                     seg(_lib.MODE_CONS, t, SEG_ROW, tp.nrec)
+        # experiment knob: keep only heavy (k > 2) or only light segments
+        filt = os.environ.get("EXA_SEG_FILTER")
+        if filt:
+            for m in segs:
+                segs[m] = [sg for sg in segs[m]
+                           if (terms[sg[0]].tape.k > 2) == (filt == "heavy") or sg[1] != SEG_TERM and filt == "light"]
+        # Each callback -> a heavy kernel (patterns with transcendentals or > 2
+        # slots, small CTAs so the few heavy CTAs spread evenly over the 148
+        # SMs) and a light kernel (everything else, big CTAs, few registers);
+        # kernel id = 2 * mode + {0 heavy, 1 light}.  They run concurrently.
         self.segs = {}
         self.n_ctas = []
         for m in range(_lib.NMODES):
-            cta = 0
-            lst = []
-            for (t, kind, nrec) in segs[m]:
-                lst.append((t, kind, cta, nrec))
-                cta += (nrec + THREADS - 1) // THREADS
-            self.segs[m] = lst
-            self.n_ctas.append(cta)
+            for half in (0, 1):
+                kid = 2 * m + half
+                th = self.threads[half]
+                cta = 0
+                lst = []
+                for (t, kind, nrec) in segs[m]:
+                    heavy = SPLIT_HEAVY and kind == SEG_TERM and pcs[self.term_pid[t]].heavy
+                    if heavy != (half == 0):
+                        continue
+                    rpt = pcs[self.term_pid[t]].rpt if kind == SEG_TERM else 1
+                    lst.append((t, kind, cta, nrec, rpt))
+                    cta += (nrec + th * rpt - 1) // (th * rpt)
+                self.segs[kid] = lst
+                self.n_ctas.append(cta)
 
         # ---- objective program ---------------------------------------------
         leaves: list = []
@@ -337,7 +359,7 @@ class HostLayout:
 
 def host_layout(plan) -> HostLayout:
     lay = getattr(plan, "_exa_layout", None)
-    if lay is None or lay.threads != THREADS:
+    if lay is None or lay.threads != (THREADS_HEAVY, THREADS):
         lay = HostLayout(plan)
         plan._exa_layout = lay
     return lay
@@ -381,11 +403,11 @@ class DevicePlan:
                       "row_offset", "cons_direct", "k", "jac0", "hess0", "scr0"):
                 setattr(td, k, d[k])
         seg_arrays = []
-        for m in range(_lib.NMODES):
+        for m in range(_lib.NKERN):
             lst = lay.segs[m]
             arr = (_lib.SegDesc * max(1, len(lst)))()
-            for s, (t, kind, cta0, nrec) in enumerate(lst):
-                arr[s].term, arr[s].kind, arr[s].cta0, arr[s].nrec = t, kind, cta0, nrec
+            for s, (t, kind, cta0, nrec, rpt) in enumerate(lst):
+                arr[s].term, arr[s].kind, arr[s].cta0, arr[s].nrec = t, kind | (rpt << 8), cta0, nrec
             seg_arrays.append(arr)
 
         desc = _lib.PlanDesc()
@@ -399,8 +421,8 @@ class DevicePlan:
         desc.n_i32 = lay.i32.size
         desc.terms = C.cast(descs, C.POINTER(_lib.TermDesc))
         desc.n_terms = len(terms)
-        desc.threads = lay.threads
-        for m in range(_lib.NMODES):
+        desc.threads[0], desc.threads[1] = lay.threads
+        for m in range(_lib.NKERN):
             desc.segs[m] = C.cast(seg_arrays[m], C.POINTER(_lib.SegDesc))
             desc.n_segs[m] = len(lay.segs[m])
             desc.n_ctas[m] = lay.n_ctas[m]
@@ -438,7 +460,9 @@ class DevicePlan:
         _lib.check(self._lib.exa_plan_info(self.handle, C.byref(b), C.byref(r)), "plan_info")
         return {"device_bytes": b.value, "regs_set_kernel": r.value, "patterns": len(self.patterns),
                 "specialised": self.layout.specialised,
-                "ctas": dict(zip(("set", "cons", "jac", "hess", "objv", "grad"), self.n_ctas))}
+                "ctas": {f"{m}_{h}": self.n_ctas[2 * i + j]
+                         for i, m in enumerate(("set", "cons", "jac", "hess", "objv", "grad"))
+                         for j, h in enumerate(("h", "l"))}}
 
     def __del__(self):
         h = getattr(self, "handle", None)

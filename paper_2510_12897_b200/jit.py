@@ -25,10 +25,12 @@ CSRC = Path(__file__).resolve().parent / "csrc"
 CACHE_DIR = Path(os.environ.get("EXA_JIT_CACHE", Path(__file__).resolve().parent / "_jit"))
 NVRTC_OPTIONS = ("-arch=sm_100a", "--fmad=false", "-default-device", "-std=c++17", "-lineinfo",
                  "--extra-device-vectorization")
-THREADS = int(os.environ.get("EXA_THREADS", "256"))
+THREADS = int(os.environ.get("EXA_THREADS", "256"))  # light kernels
+THREADS_HEAVY = int(os.environ.get("EXA_THREADS_HEAVY", "128"))  # heavy kernels
 # tuning knobs (experiments only; defaults are the product configuration)
 MIN_BLOCKS = int(os.environ.get("EXA_MINB", "0"))
-SINCOS_IMPL = os.environ.get("EXA_SINCOS_IMPL", "cr")  # "cuda" = libdevice sincos, NOT parity-exact
+SINCOS_IMPL = os.environ.get("EXA_SINCOS_IMPL", "cr")
+PDL = os.environ.get("EXA_PDL", "0") == "1"  # must match the library's launch attribute  # "cuda" = libdevice sincos, NOT parity-exact
 
 _lock = threading.Lock()
 _mem_cache: dict = {}
@@ -62,6 +64,15 @@ __device__ __forceinline__ void exa_report(const ExaArgs& A, int rank, int instr
 #define EXA_REC_ALL 0
 #define EXA_REC_FIRST 1
 #define EXA_DOMAIN_AT(instr, rec1) exa_report(A, rank, (instr), (rec1))
+// programmatic dependent launch: release the next kernel early; wait for the
+// previous one before the first access to caller memory (x, y, outputs)
+#if EXA_PDL
+#define EXA_GRID_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define EXA_GRID_RELEASE() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+#else
+#define EXA_GRID_WAIT() do {} while (0)
+#define EXA_GRID_RELEASE() do {} while (0)
+#endif
 """
 
 _COMMON = r"""
@@ -90,6 +101,7 @@ __device__ __forceinline__ int exa_rank(const ExaTerm& T, const ExaArgs& A) {
 // (reference autodiff.py:573-580).  val(term, record) evaluates one record.
 template <class VAL>
 __device__ __forceinline__ void exa_row(const ExaTerm& T, int r, const ExaArgs& A, VAL val) {
+  EXA_GRID_WAIT();
   double acc = 0.0 + exa_dispatch_val(T, r, A, exa_rank(T, A));
   const int e1 = __ldg(T.row_ptr + r + 1);
   for (int e = __ldg(T.row_ptr + r); e < e1; ++e) {
@@ -108,6 +120,7 @@ template <class VAL>
 __device__ __forceinline__ void exa_rowfold(const ExaTerm& T, int slot, const ExaArgs& A, VAL val) {
   const int lane = threadIdx.x & 31;
   const int2 e = __ldg(reinterpret_cast<const int2*>(T.row_ent) + slot);
+  EXA_GRID_WAIT();
   const bool pad = e.x < 0;
   const int p = pad ? 0 : (e.x >> 16);
   const double v = pad ? 0.0 : val(e.x & 0xffff, e.y);
@@ -147,37 +160,47 @@ __device__ __forceinline__ void exa_kernel_body(const ExaTerm* __restrict__ term
 #else
   const ExaSeg sg = segs[__ldg(cta_seg + blockIdx.x)];
 #endif
-  const int r = (int)(blockIdx.x - sg.cta0) * (int)blockDim.x + (int)threadIdx.x;
-  if (r >= sg.nrec) return;
+  const int kind = sg.kind & 0xff, rpt = sg.kind >> 8;
   const ExaTerm& T = EXA_TERM(sg.term);
   auto val = [&](int t, int rec) -> double {
     const ExaTerm& U = EXA_TERM(t);
     return exa_dispatch_val(U, rec, A, exa_rank(U, A));
   };
-  if (sg.kind == EXA_SEG_FOLD) {
-    exa_rowfold(T, r, A, val);
-  } else if (sg.kind == EXA_SEG_ROW) {
-    exa_row(T, r, A, val);
-  } else {
-    exa_dispatch_term<MODE>(T, r, A, exa_rank(T, A));
+  const int r0 = (int)(blockIdx.x - sg.cta0) * (int)blockDim.x * rpt + (int)threadIdx.x;
+  if (kind == EXA_SEG_TERM) {
+    for (int q = 0; q < rpt; ++q) {
+      const int r = r0 + q * (int)blockDim.x;
+      if (r < sg.nrec) exa_dispatch_term<MODE>(T, r, A, exa_rank(T, A));
+    }
+    return;
   }
+  if (r0 >= sg.nrec) return;
+  if (kind == EXA_SEG_FOLD) exa_rowfold(T, r0, A, val);
+  else exa_row(T, r0, A, val);
 }
 """
 
 _ENTRIES = r"""
-#define EXA_ENTRY(NAME, MODE)                                                                  \
-  extern "C" __global__ void __launch_bounds__(@BOUNDS@) NAME(                                \
+#define EXA_ENTRY(NAME, MODE, BOUNDS)                                                          \
+  extern "C" __global__ void __launch_bounds__(BOUNDS) NAME(                                  \
       const ExaTerm* __restrict__ terms, const ExaSeg* __restrict__ segs,                     \
       const int* __restrict__ cta_seg, ExaArgs A) {                                           \
+    EXA_GRID_RELEASE();                                                                        \
     exa_kernel_body<MODE>(terms, segs, cta_seg, A);                                            \
   }
 
-EXA_ENTRY(exa_k_set, EXA_M_CONS | EXA_M_JAC | EXA_M_HESS)
-EXA_ENTRY(exa_k_cons, EXA_M_CONS)
-EXA_ENTRY(exa_k_jac, EXA_M_JAC)
-EXA_ENTRY(exa_k_hess, EXA_M_HESS)
-EXA_ENTRY(exa_k_objv, EXA_M_OBJV)
-EXA_ENTRY(exa_k_grad, EXA_M_GRAD)
+EXA_ENTRY(exa_k_set_h, EXA_M_CONS | EXA_M_JAC | EXA_M_HESS, @BOUNDS_H@)
+EXA_ENTRY(exa_k_set_l, EXA_M_CONS | EXA_M_JAC | EXA_M_HESS, @BOUNDS_L@)
+EXA_ENTRY(exa_k_cons_h, EXA_M_CONS, @BOUNDS_H@)
+EXA_ENTRY(exa_k_cons_l, EXA_M_CONS, @BOUNDS_L@)
+EXA_ENTRY(exa_k_jac_h, EXA_M_JAC, @BOUNDS_H@)
+EXA_ENTRY(exa_k_jac_l, EXA_M_JAC, @BOUNDS_L@)
+EXA_ENTRY(exa_k_hess_h, EXA_M_HESS, @BOUNDS_H@)
+EXA_ENTRY(exa_k_hess_l, EXA_M_HESS, @BOUNDS_L@)
+EXA_ENTRY(exa_k_objv_h, EXA_M_OBJV, @BOUNDS_H@)
+EXA_ENTRY(exa_k_objv_l, EXA_M_OBJV, @BOUNDS_L@)
+EXA_ENTRY(exa_k_grad_h, EXA_M_GRAD, @BOUNDS_H@)
+EXA_ENTRY(exa_k_grad_l, EXA_M_GRAD, @BOUNDS_L@)
 """
 
 _MODE_BITS = ("EXA_M_CONS | EXA_M_JAC | EXA_M_HESS", "EXA_M_CONS", "EXA_M_JAC", "EXA_M_HESS",
@@ -221,27 +244,35 @@ def _specialised_kernels(layout) -> str:
       default: return 0.0;
   }}
 }}""")
-    threads = layout.threads
     for m, name in enumerate(KERNEL_NAMES):
-        body = [f"extern \"C\" __global__ void __launch_bounds__(@BOUNDS@) {name}(",
-                "    const ExaTerm* __restrict__ terms, const ExaSeg* __restrict__ segs,",
-                "    const int* __restrict__ cta_seg, ExaArgs A) {",
-                "  const int b = (int)blockIdx.x;"]
-        for (t, kind, cta0, nrec) in layout.mode_segments(m):
-            n_cta = (nrec + threads - 1) // threads
-            body.append(f"  if (b < {cta0 + n_cta}) {{")
-            body.append(f"    const int r = (b - {cta0}) * {threads} + (int)threadIdx.x;")
-            body.append(f"    if (r >= {nrec}) return;")
-            body.append(f"    ExaTerm T; exa_init_T{t}(T, A);")
-            if kind == 0:
-                body.append(f"    exa_term_{layout.term_pid[t]}<{_MODE_BITS[m]}>(T, r, A, exa_rank(T, A));")
-            else:
-                fn = "exa_rowfold" if kind == 2 else "exa_row"
-                body.append(f"    {fn}(T, r, A, [&](int u, int rec) {{ return exa_rowval_T{t}(u, rec, A); }});")
-            body.append("    return;")
-            body.append("  }")
-        body.append("}")
-        out.append("\n".join(body))
+        for half, suffix in ((0, "_h"), (1, "_l")):
+            kid = 2 * m + half
+            threads = layout.threads[half]
+            body = [f"extern \"C\" __global__ void __launch_bounds__(@BOUNDS_{'H' if half == 0 else 'L'}@) {name}{suffix}(",
+                    "    const ExaTerm* __restrict__ terms, const ExaSeg* __restrict__ segs,",
+                    "    const int* __restrict__ cta_seg, ExaArgs A) {",
+                    "  EXA_GRID_RELEASE();",
+                    "  const int b = (int)blockIdx.x;"]
+            for (t, kind, cta0, nrec, rpt) in layout.mode_segments(kid):
+                n_cta = (nrec + threads * rpt - 1) // (threads * rpt)
+                body.append(f"  if (b < {cta0 + n_cta}) {{")
+                body.append(f"    ExaTerm T; exa_init_T{t}(T, A);")
+                if kind == 0:
+                    body.append(f"    const int r0 = (b - {cta0}) * {threads * rpt} + (int)threadIdx.x;")
+                    body.append("#pragma unroll")
+                    body.append(f"    for (int q = 0; q < {rpt}; ++q) {{")
+                    body.append(f"      const int r = r0 + q * {threads};")
+                    body.append(f"      if (r < {nrec}) exa_term_{layout.term_pid[t]}<{_MODE_BITS[m]}>(T, r, A, exa_rank(T, A));")
+                    body.append("    }")
+                else:
+                    body.append(f"    const int r = (b - {cta0}) * {threads} + (int)threadIdx.x;")
+                    body.append(f"    if (r >= {nrec}) return;")
+                    fn = "exa_rowfold" if kind == 2 else "exa_row"
+                    body.append(f"    {fn}(T, r, A, [&](int u, int rec) {{ return exa_rowval_T{t}(u, rec, A); }});")
+                body.append("    return;")
+                body.append("  }")
+            body.append("}")
+            out.append("\n".join(body))
     return "\n\n".join(out)
 
 
@@ -259,6 +290,7 @@ def module_source(patterns, meta_const: bool = True, layout=None) -> str:
     seen: set = set()
     parts = ["// generated by paper_2510_12897_b200.jit",
              f"#define EXA_META_CONST {1 if (meta_const and layout is None) else 0}",
+             f"#define EXA_PDL {1 if PDL else 0}",
              _inline_header("exa_device.h", seen), _inline_header("exa_math.h", seen), _PRELUDE]
     if SINCOS_IMPL == "cuda":
         parts.append("#define exa_sincos(x, s, c) sincos((x), (s), (c))")
@@ -274,8 +306,8 @@ def module_source(patterns, meta_const: bool = True, layout=None) -> str:
         parts.append(_ENTRIES)
     else:
         parts.append(_specialised_kernels(layout))
-    bounds = f"{THREADS}, {MIN_BLOCKS}" if MIN_BLOCKS else str(THREADS)
-    return "\n".join(parts).replace("@BOUNDS@", bounds)
+    bl = f"{THREADS}, {MIN_BLOCKS}" if MIN_BLOCKS else str(THREADS)
+    return "\n".join(parts).replace("@BOUNDS_L@", bl).replace("@BOUNDS_H@", str(THREADS_HEAVY))
 
 
 def compile_module(src: str) -> bytes:

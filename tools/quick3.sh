@@ -1,0 +1,9 @@
+#!/bin/bash
+TAG=${1:-q}
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_gpu_tests.log 2>&1
+OUT=gpurun_out/${TAG}_timing.jsonl; : > $OUT
+for th in 128 64 96 256; do EXA_THREADS_HEAVY=$th timeout 300 python tools/set_timing.py case13659 set >> $OUT 2>> gpurun_out/${TAG}_timing.err; done
+EXA_SEG_FILTER=heavy timeout 300 python tools/set_timing.py case13659 set >> $OUT 2>> gpurun_out/${TAG}_timing.err
+EXA_SEG_FILTER=light timeout 300 python tools/set_timing.py case13659 set >> $OUT 2>> gpurun_out/${TAG}_timing.err
+for m in cons jac hess; do timeout 300 python tools/set_timing.py case13659 $m >> $OUT 2>> gpurun_out/${TAG}_timing.err; done
+echo done

@@ -78,4 +78,4 @@ us = e0.elapsed_time(e1) * 1e3 / (5 * S * R)
 info = plans[0].info()
 print(json.dumps({"workload": name, "mode": mode, "threads": jit.THREADS, "minb": jit.MIN_BLOCKS,
                   "sincos": jit.SINCOS_IMPL, "us_per_set": us, "GBps": bps / us / 1e3,
-                  "regs": info["regs_set_kernel"], "ctas": info["ctas"]["set"], "jit_s": tjit}), flush=True)
+                  "regs": info["regs_set_kernel"], "ctas": info["ctas"], "jit_s": tjit}), flush=True)
