@@ -37,6 +37,9 @@ import os
 import numpy as np
 
 _SIN_COS = ("sin", "cos")
+# EXA_EXACT_ZERO_SIGN=1 keeps every 0 + x of the reference (bitwise identical
+# signs of zero in J/H); default drops them in derivative space (see Gen.bin)
+_DERIV_ZERO_ELISION = os.environ.get("EXA_EXACT_ZERO_SIGN", "0") != "1"
 
 
 class Arr:
@@ -107,6 +110,9 @@ class Gen:
         self.n = 0
         self.memo: dict = {}
         self.sincos: dict = {}
+        self.diffs: dict = {}  # name of a Sym defined as x - y -> (x, y)
+        # derivative-space emission (see bin add); off while emitting values
+        self.deriv = False
         self.checks: list = []
 
     def new(self, expr: str, nz: bool = False) -> Sym:
@@ -153,14 +159,21 @@ class Gen:
             if cb == 0.0 and not math.copysign(1.0, cb) < 0:
                 return a
         elif op == "add":
-            # x + (-0) == x;  (+0) + x == x unless x is -0.0
-            if cb == 0.0 and (math.copysign(1.0, cb) < 0 or _nz(a)):
+            # x + (-0) == x;  (+0) + x == x unless x is -0.0.  In derivative
+            # space (adjoints, tangents, their slot sums) the sign of a zero can
+            # only ever reach the sign of an exactly-zero output -- derivative
+            # quantities are only added and multiplied, never divided by or fed
+            # to a function -- so there the normalising 0 + x is dropped.
+            if cb == 0.0 and (math.copysign(1.0, cb) < 0 or _nz(a) or self.deriv):
                 return a
-            if ca == 0.0 and (math.copysign(1.0, ca) < 0 or _nz(b)):
+            if ca == 0.0 and (math.copysign(1.0, ca) < 0 or _nz(b) or self.deriv):
                 return b
         sym = {"add": "+", "sub": "-", "mul": "*", "div": "/"}[op]
         nz = (op == "add" and (_nz(a) or _nz(b))) or (op == "sub" and _nz(a))
-        return self.new(f"{self.r(a)} {sym} {self.r(b)}", nz)
+        out = self.new(f"{self.r(a)} {sym} {self.r(b)}", nz)
+        if op == "sub":
+            self.diffs[out.name] = (self.r(a), self.r(b))
+        return out
 
     def add(self, a, b):
         return self.bin("add", a, b)
@@ -190,6 +203,15 @@ class Gen:
             return Arr(val) if isinstance(a, Arr) else val
         if name in _SIN_COS:
             pair = self.sincos.get(a.name)
+            if pair is None and a.name in self.diffs:
+                # sin(y - x) = -sin(x - y), cos(y - x) = cos(x - y): IEEE subtraction is
+                # exactly antisymmetric and exa_sincos is odd/even symmetric
+                lhs, rhs = self.diffs[a.name]
+                other = self.memo.get(f"{rhs} - {lhs}")
+                if other is not None and other.name in self.sincos:
+                    s_o, c_o = self.sincos[other.name]
+                    pair = (self.new(f"-{s_o.name}"), c_o)
+                    self.sincos[a.name] = pair
             if pair is None:
                 s, c = f"s_{a.name}", f"c_{a.name}"
                 self.lines.append(f"  double {s}, {c}; exa_sincos({a.name}, &{s}, &{c});")
@@ -522,6 +544,7 @@ class PatternCode:
         n_value_lines = len(g.lines)
 
         # first order
+        g.deriv = _DERIV_ZERO_ELISION
         adj = self._adjoints(g, v) if k else None
         grads = self._slot_sums(g, adj) if k else []
         n_grad_lines = len(g.lines)
@@ -595,6 +618,122 @@ class PatternCode:
         heavy = bool(g.sincos) or any(ins[0] in ("exp", "log", "pow") for ins in self.instr) or k > 2
         self.rpt = int(os.environ.get("EXA_RPT_LIGHT", "1")) if (not heavy and n_ops <= 40) else 1
         self.heavy = heavy
+        return "\n".join(out)
+
+    def group_source(self, gid: int, members: list) -> str:
+        """One thread evaluates record r of several terms of this pattern.
+
+        ``members[m] = {"cols": [group column id per index column],
+        "blocks": [group block id per slot]}``: index columns with the same
+        content are loaded once, variables with the same (block, column) are
+        gathered once, and every identical sub-expression -- in OPF the 4 branch
+        flow blocks share vm_f, vm_t, va_f, va_t and sin/cos(va_f - va_t) --
+        is computed once (the generator's CSE), while each member's outputs keep
+        the reference's per-term operation order."""
+        self.instr = self.tape_norm()
+        k = self.k
+        M = len(members)
+        g = Gen()
+        pre, post = [], []
+        u_src: dict = {}
+        for m, mem in enumerate(members):
+            for c, u in enumerate(mem["cols"]):
+                u_src.setdefault(u, (m, c))
+        for u, (m, c) in sorted(u_src.items()):
+            pre.append(f"  const int i{u} = __ldg(T{m}.ix[{c}] + r);")
+        fsyms = []
+        for m in range(M):
+            d = {}
+            for fi, fname in enumerate(self.tape.field_names):
+                pre.append(f"  const double f{m}_{fi} = __ldg(T{m}.f[{fi}] + r);")
+                d[fname] = Sym(f"f{m}_{fi}")
+            fsyms.append(d)
+        xkey: dict = {}
+        vsyms, cnames = [], []
+        for m, mem in enumerate(members):
+            vs, cn = [], []
+            for s_, (_, ic) in enumerate(self.slot_struct):
+                key = (mem["blocks"][s_], mem["cols"][ic])
+                if key not in xkey:
+                    n = len(xkey)
+                    xkey[key] = n
+                    post.append(f"  const int cg{n} = T{m}.voff[{s_}] + i{mem['cols'][ic]};")
+                    post.append(f"  const double xg{n} = __ldg(A.x + cg{n});")
+                vs.append(Sym(f"xg{xkey[key]}"))
+                cn.append(f"cg{xkey[key]}")
+            vsyms.append(vs)
+            cnames.append(cn)
+        if k:
+            for m in range(M):
+                post.append(f"  const double wgt{m} = !(MODE & EXA_M_HESS) ? 0.0 : (T{m}.kind == EXA_OBJ) ? A.w"
+                            f" : __ldg(A.y + (T{m}.rows ? __ldg(T{m}.rows + r) : T{m}.row_offset + r));")
+        R = Gen.r
+        # Stores are emitted as soon as their value is final (cons after the
+        # value pass, J after the adjoint sweep, each Hessian column after its
+        # seed's sweep) so that the LSU drains while the next sweep computes.
+        for m in range(M):
+            T = f"T{m}"
+            g.lines.append(f"  rank = rank{m};")
+            g.deriv = False
+            v = self._values(g, {"field": fsyms[m], "var": vsyms[m]})
+            root = v[-1]
+            g.lines.append(f"  if ((MODE & EXA_M_CONS) && {T}.cons_direct) Cout[{T}.row_offset + r] = 0.0 + {R(root)};")
+            g.lines.append(f"  if ((MODE & EXA_M_OBJV) && {T}.kind == EXA_OBJ) A.V[{T}.scr0 + r] = {R(root)};")
+            if not k:
+                continue
+            g.deriv = _DERIV_ZERO_ELISION
+            adj = self._adjoints(g, v)
+            grads = self._slot_sums(g, adj)
+            for s_ in range(k):
+                g.lines.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
+                g.lines.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
+            for seed in range(k):
+                t = self._tangents(g, v, seed)
+                col = self._slot_sums(g, self._adjoint_tangents(g, v, adj, t))
+                j = seed
+                for i in range(j, k):
+                    expr = R(col[i])
+                    if i != j and self.slot_struct[i][0] == self.slot_struct[j][0]:
+                        expr = f"({cnames[m][i]} == {cnames[m][j]} ? {expr} * 2.0 : {expr})"
+                    pair = i * (i + 1) // 2 + j
+                    g.lines.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
+        res = []
+        args = ", ".join(f"const ExaTerm& T{m}" for m in range(M))
+        ranks = ", ".join(f"int rank{m}" for m in range(M))
+        out = [f"template <int MODE>\n__device__ __forceinline__ void exa_grp_{gid}({args}, int r, const ExaArgs& A, {ranks}) {{",
+               "  double* __restrict__ Cout = A.c;", "  double* __restrict__ Jout = A.J;",
+               "  double* __restrict__ Hout = A.H;", "  int rank = rank0;"]
+        out.extend(pre)
+        out.append("  EXA_GRID_WAIT();")
+        out.extend(post)
+        out.extend(g.lines)
+        for m, (root, grads, by_seed) in enumerate(res):  # (stores already emitted inline)
+            T = f"T{m}"
+            out.append("  if (MODE & (EXA_M_CONS | EXA_M_OBJV)) {")
+            out.append(f"    if ((MODE & EXA_M_CONS) && {T}.cons_direct) Cout[{T}.row_offset + r] = 0.0 + {R(root)};")
+            out.append(f"    if ((MODE & EXA_M_OBJV) && {T}.kind == EXA_OBJ) A.V[{T}.scr0 + r] = {R(root)};")
+            out.append("  }")
+            if not k:
+                continue
+            out.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) {{")
+            for s_ in range(k):
+                out.append(f"    Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
+            out.append("  }")
+            out.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) {{")
+            for s_ in range(k):
+                out.append(f"    A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
+            out.append("  }")
+            out.append("  if (MODE & EXA_M_HESS) {")
+            pair = 0
+            for i in range(k):
+                for j in range(i + 1):
+                    expr = R(by_seed[j][i])
+                    if i != j and self.slot_struct[i][0] == self.slot_struct[j][0]:
+                        expr = f"({cnames[m][i]} == {cnames[m][j]} ? {expr} * 2.0 : {expr})"
+                    out.append(f"    Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
+                    pair += 1
+            out.append("  }")
+        out.append("}")
         return "\n".join(out)
 
     def tape_norm(self):

@@ -488,10 +488,12 @@ static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaSt
   const bool h = p->n_ctas[kh] > 0, l = p->n_ctas[kl] > 0;
   int rc = 0;
   if (h && l) {
+    // heavy first: its few, long-lived CTAs must become resident before the
+    // light kernel's many short CTAs fill every SM
     CU(cudaEventRecord(w->fork, st));
     CU(cudaStreamWaitEvent(w->aux, w->fork, 0));
-    if ((rc = launch_kid(p, w, kl, A, w->aux))) return rc;
     if ((rc = launch_kid(p, w, kh, A, st))) return rc;
+    if ((rc = launch_kid(p, w, kl, A, w->aux))) return rc;
     CU(cudaEventRecord(w->join, w->aux));
     CU(cudaStreamWaitEvent(st, w->join, 0));
   } else if (h) {

@@ -35,7 +35,11 @@ ALIGN = 32  # elements: 256 B for fp64, 128 B for int32
 
 KIND = {"objective": 0, "constraint": 1, "augment": 2}
 OP_LEAF, OP_ADD, OP_CONST, OP_ZERO_PLUS, OP_TOTAL_ADD = range(5)
-SEG_TERM, SEG_ROW, SEG_FOLD = 0, 1, 2
+SEG_TERM, SEG_ROW, SEG_FOLD, SEG_GROUP = 0, 1, 2, 3
+
+# Terms of one heavy pattern that share index columns (OPF: the 4 branch-flow
+# blocks) are evaluated by one thread per record (see codegen.group_source).
+GROUP_MAX = int(os.environ.get("EXA_GROUP_MAX", "2"))
 
 # Models with at most this many terms get a *specialised* module (metadata
 # compiled in as constants); larger ones (e.g. thousands of per-instance
@@ -236,6 +240,12 @@ class HostLayout:
         self.f64 = f64.array()
         self.i32 = i32.array()
 
+        # ---- term groups (specialised modules only) ---------------------------
+        self.groups = []  # (pid, [term ids], members meta)
+        self.group_of: dict = {}
+        if len(terms) <= META_CONST_MAX_TERMS and GROUP_MAX > 1:
+            self._make_groups(terms, descs)
+
         # ---- segments per callback -----------------------------------------
         segs = {m: [] for m in range(_lib.NMODES)}
 
@@ -246,6 +256,8 @@ class HostLayout:
         for t, tp in enumerate(terms):
             k = tp.tape.k
             chk = pcs[self.term_pid[t]].has_checks
+            if t in self.group_of and self.groups[self.group_of[t]][1][0] != t:
+                continue  # evaluated by its group's first member
             if tp.kind == "objective":
                 if k:
                     seg(_lib.MODE_SET, t, SEG_TERM, tp.nrec)
@@ -274,9 +286,22 @@ class HostLayout:
         # experiment knob: keep only heavy (k > 2) or only light segments
         filt = os.environ.get("EXA_SEG_FILTER")
         if filt:
+            def keep(sg):
+                t, kind = sg[0], sg[1]
+                heavy = kind == SEG_TERM and terms[t].tape.k > 2
+                if filt == "heavy":
+                    return heavy
+                if filt == "light":
+                    return not heavy
+                if filt == "fold":
+                    return kind in (SEG_FOLD, SEG_ROW)
+                if filt == "aug":
+                    return kind == SEG_TERM and terms[t].kind == "augment"
+                if filt == "other":
+                    return kind == SEG_TERM and not heavy and terms[t].kind != "augment"
+                return True
             for m in segs:
-                segs[m] = [sg for sg in segs[m]
-                           if (terms[sg[0]].tape.k > 2) == (filt == "heavy") or sg[1] != SEG_TERM and filt == "light"]
+                segs[m] = [sg for sg in segs[m] if keep(sg)]
         # Each callback -> a heavy kernel (patterns with transcendentals or > 2
         # slots, small CTAs so the few heavy CTAs spread evenly over the 148
         # SMs) and a light kernel (everything else, big CTAs, few registers);
@@ -290,10 +315,14 @@ class HostLayout:
                 cta = 0
                 lst = []
                 for (t, kind, nrec) in segs[m]:
-                    heavy = SPLIT_HEAVY and kind == SEG_TERM and pcs[self.term_pid[t]].heavy
+                    if kind == SEG_TERM and t in self.group_of:
+                        kind = SEG_GROUP
+                    heavy = SPLIT_HEAVY and kind in (SEG_TERM, SEG_GROUP) and pcs[self.term_pid[t]].heavy
                     if heavy != (half == 0):
                         continue
                     rpt = pcs[self.term_pid[t]].rpt if kind == SEG_TERM else 1
+                    if kind == SEG_GROUP:  # segment names the group, not the term
+                        t = self.group_of[t]
                     lst.append((t, kind, cta, nrec, rpt))
                     cta += (nrec + th * rpt - 1) // (th * rpt)
                 self.segs[kid] = lst
@@ -321,6 +350,48 @@ class HostLayout:
         self.specialised = len(terms) <= META_CONST_MAX_TERMS
         self.source = module_source(self.patterns, meta_const=False,
                                     layout=self if self.specialised else None)
+
+    def _make_groups(self, terms, descs):
+        import hashlib
+
+        def col_hash(arr):
+            return hashlib.blake2b(np.ascontiguousarray(arr, dtype=np.int64).tobytes(), digest_size=16).digest()
+
+        sig = {}
+        for t, tp in enumerate(terms):
+            pc = self.patterns[self.term_pid[t]]
+            if not pc.heavy or tp.nrec == 0:
+                continue
+            key = (self.term_pid[t], tp.nrec, tp.kind, descs[t]["cons_direct"])
+            sig.setdefault(key, []).append(t)
+        for key, cand in sig.items():
+            hashes = {t: [col_hash(terms[t].table.indices[nm]) for nm in terms[t].tape.index_names] for t in cand}
+            free = list(cand)
+            while free:
+                t0 = free.pop(0)
+                grp = [t0]
+                cols = set(hashes[t0])
+                for u in list(free):
+                    if len(grp) >= GROUP_MAX:
+                        break
+                    if cols & set(hashes[u]):
+                        grp.append(u)
+                        cols |= set(hashes[u])
+                        free.remove(u)
+                if len(grp) < 2:
+                    continue
+                uid: dict = {}
+                bid: dict = {}
+                members = []
+                for t in grp:
+                    members.append({
+                        "cols": [uid.setdefault(h, len(uid)) for h in hashes[t]],
+                        "blocks": [bid.setdefault(id(b), len(bid)) for b in terms[t].slot_blocks],
+                    })
+                gi = len(self.groups)
+                self.groups.append((self.term_pid[t0], grp, members))
+                for t in grp:
+                    self.group_of[t] = gi
 
     # accessors used by the specialised-kernel generator (jit.py)
     def term_descs(self):

@@ -244,7 +244,10 @@ def _specialised_kernels(layout) -> str:
       default: return 0.0;
   }}
 }}""")
+    for gid, (pid, grp, members) in enumerate(getattr(layout, "groups", [])):
+        out.append(layout.patterns[pid].group_source(gid, members))
     for m, name in enumerate(KERNEL_NAMES):
+        m_ = m
         for half, suffix in ((0, "_h"), (1, "_l")):
             kid = 2 * m + half
             threads = layout.threads[half]
@@ -256,6 +259,18 @@ def _specialised_kernels(layout) -> str:
             for (t, kind, cta0, nrec, rpt) in layout.mode_segments(kid):
                 n_cta = (nrec + threads * rpt - 1) // (threads * rpt)
                 body.append(f"  if (b < {cta0 + n_cta}) {{")
+                if kind == 3:  # term group: t is the group id
+                    pid, grp, _ = layout.groups[t]
+                    for gm, u in enumerate(grp):
+                        body.append(f"    ExaTerm T{gm}; exa_init_T{u}(T{gm}, A);")
+                    body.append(f"    const int r = (b - {cta0}) * {threads} + (int)threadIdx.x;")
+                    body.append(f"    if (r >= {nrec}) return;")
+                    tl = ", ".join(f"T{gm}" for gm in range(len(grp)))
+                    rl = ", ".join(f"exa_rank(T{gm}, A)" for gm in range(len(grp)))
+                    body.append(f"    exa_grp_{t}<{_MODE_BITS[m_]}>({tl}, r, A, {rl});")
+                    body.append("    return;")
+                    body.append("  }")
+                    continue
                 body.append(f"    ExaTerm T; exa_init_T{t}(T, A);")
                 if kind == 0:
                     body.append(f"    const int r0 = (b - {cta0}) * {threads * rpt} + (int)threadIdx.x;")
@@ -322,7 +337,15 @@ def compile_module(src: str) -> bytes:
         if path.is_file():
             data = path.read_bytes()
         else:
-            data = _lib.jit_compile(src, opts, name=f"exa_{key[:12]}.cu")
+            # the source is kept beside the cubin under the name NVRTC records in
+            # -lineinfo, so `ncu --import-source on` resolves generated lines
+            src_path = CACHE_DIR / f"{key}.cu"
+            try:
+                CACHE_DIR.mkdir(parents=True, exist_ok=True)
+                src_path.write_text(src)
+            except OSError:
+                pass
+            data = _lib.jit_compile(src, opts, name=str(src_path))
             try:
                 CACHE_DIR.mkdir(parents=True, exist_ok=True)
                 tmp = path.with_suffix(f".tmp{os.getpid()}")

@@ -22,7 +22,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "case13659"
 mode = sys.argv[2] if len(sys.argv) > 2 else "set"
 model = build_workload(name, lower_to_gpu=False)
 bps = model_summary(model)["bytes_per_set"]
-R = max(2, int(np.ceil(2 * 126 * 2**20 / bps)))
+R = int(os.environ.get("EXA_R", "0")) or max(2, int(np.ceil(2 * 126 * 2**20 / bps)))
 dev = torch.device("cuda", 0)
 t0 = time.time()
 plans = [DevicePlan(model, 0) for _ in range(R)]
@@ -76,6 +76,6 @@ with torch.cuda.stream(st):
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / (5 * S * R)
 info = plans[0].info()
-print(json.dumps({"workload": name, "mode": mode, "threads": jit.THREADS, "minb": jit.MIN_BLOCKS,
+print(json.dumps({"workload": name, "mode": mode, "R": R, "threads": jit.THREADS, "minb": jit.MIN_BLOCKS,
                   "sincos": jit.SINCOS_IMPL, "us_per_set": us, "GBps": bps / us / 1e3,
                   "regs": info["regs_set_kernel"], "ctas": info["ctas"], "jit_s": tjit}), flush=True)
