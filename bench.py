@@ -9,8 +9,12 @@ One *step* = ``--sets-per-step`` (default 64) callback sets, each a full
 evaluation point, executed as ONE fused kernel launch per set.  Steps are
 replayed from a CUDA graph.  L2 (126 MB) is defeated by rotating over R
 replicas of the whole working set (plan parameters + x + y + outputs) whose
-total exceeds 2x the L2 size.  N > 1 (torchrun): every rank evaluates its own
-scenario stream (weak scaling, no data-path collective); time = max over ranks.
+total exceeds 2x the L2 size.  N > 1 (torchrun): for the single-instance
+configs (default case13659) every rank evaluates its own scenario stream (weak
+scaling, no data-path collective); for the batched configs
+(``--workload mp96_case1354`` / ``n1_case2000``) each rank evaluates its
+period / instance shard of ONE instance (strong scaling; cons/jac/hess need
+no collective).  Time = max over ranks.
 """
 
 from __future__ import annotations
@@ -221,7 +225,10 @@ def main():
 
     ws, rank, local = dist_setup()
     dev = torch.device("cuda", local)
-    model = build_workload(args.workload, lower_to_gpu=False)
+    sharded = args.workload.startswith(("mp", "n1"))
+    # batched configs: this rank's shard of ONE instance (strong scaling);
+    # single-instance configs: every rank evaluates its own sets (weak scaling)
+    model = build_workload(args.workload, lower_to_gpu=False, rank=rank, world=ws if sharded else 1)
     summ = model_summary(model)
     bps = summ["bytes_per_set"]
     R = max(2, int(np.ceil(2 * L2_BYTES / bps)))
@@ -320,7 +327,7 @@ def main():
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    n_sets = args.steps * S * ws
+    n_sets = args.steps * S * (1 if sharded else ws)
     value = n_sets / (ms / 1e3)
     per_launch_s = (ms / 1e3) / (args.steps * S)
     achieved = bps / per_launch_s / 1e9
@@ -359,7 +366,7 @@ def main():
         t = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_dt = float(t.item())
-    e2e_value = n_e2e * ws / e2e_dt
+    e2e_value = n_e2e * (1 if sharded else ws) / e2e_dt
     h2d = 8 * (model.nvar + model.ncon)
     d2h = 8 * (model.ncon + model.plan.n_jac_slots + model.plan.n_hess_slots)
 
@@ -369,7 +376,7 @@ def main():
             torch.distributed.destroy_process_group()
         return
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and bps < 2e9:
         xb, yb, wb = eval_inputs(model, 0)
         cpu = cpu_baseline(model, xb, yb, wb, args.cpu_seconds, args.workload)
     info = plans[0].info()
@@ -383,7 +390,9 @@ def main():
             "hess_slots": summ["hess_slots"], "bytes_per_set": bps,
             "l2": f"rotating {R} full replicas ({R * bps / 2**20:.0f} MiB > 2x126 MiB L2)",
             "launch": "CUDA graph of single-set fused kernel launches (exa_k_set)",
-            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+            "parallelism": (f"{'period' if args.workload.startswith('mp') else 'instance'} shards x{ws}"
+                            if sharded and ws > 1 else (f"replicas x{ws}" if ws > 1 else "single GPU")),
+            "shard_bytes_per_set": bps,
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -68,25 +68,36 @@ def mpopf_shard(case, curve, rank: int, n_shards: int, corrective_action_ratio: 
 
 def attach_maps(shard: Shard, global_model) -> Shard:
     """Compute the shard -> global maps against the (host-only) global model."""
-    sm, gm = shard.model, global_model
     c0, c1, v0, v1 = shard.window
-    T = None
+    maps = attach_maps_generic(shard.model, global_model, np.arange(v0, v1), (c0, c1))
+    shard.var_map, shard.owned_vars, shard.row_map, shard.jac_map, shard.hess_map = maps
+    return shard
+
+
+def attach_maps_generic(sm, gm, local_periods, owned=None):
+    """Maps for a shard whose grid blocks hold the global periods/instances
+    ``local_periods`` (in local order); ``owned = (c0, c1)`` marks the
+    variables whose period the shard owns."""
+    local_periods = np.asarray(local_periods, dtype=np.int64)
     var_map = np.empty(sm.nvar, dtype=np.int64)
-    owned = np.zeros(sm.nvar, dtype=bool)
+    owned_mask = np.zeros(sm.nvar, dtype=bool)
     if len(sm.variables) != len(gm.variables):
         raise ModelError("shard and global models register different variable blocks")
     for sb, gb in zip(sm.variables, gm.variables):
         n = sb.shape[0]
         if len(gb.shape) == 1:  # static block: identical
             var_map[sb.offset:sb.offset + sb.size] = gb.offset + np.arange(gb.size)
-            owned[sb.offset:sb.offset + sb.size] = True
+            owned_mask[sb.offset:sb.offset + sb.size] = True
             continue
         T = gb.shape[1]
         Tv = sb.shape[1]
+        if Tv != local_periods.size:
+            raise ModelError("shard block period count does not match its period list")
         i = np.repeat(np.arange(n), Tv)
-        t = np.tile(np.arange(v0, v0 + Tv), n)
+        t = np.tile(local_periods, n)
         var_map[sb.offset:sb.offset + sb.size] = gb.offset + i * T + t
-        owned[sb.offset:sb.offset + sb.size] = (t >= c0) & (t < c1)
+        if owned is not None:
+            owned_mask[sb.offset:sb.offset + sb.size] = (t >= owned[0]) & (t < owned[1])
     sp, gp = sm.plan, gm.plan
     if len(sp.obj_terms) != len(gp.obj_terms) or len(sp.con_terms) != len(gp.con_terms):
         raise ModelError("shard and global models register different term blocks")
@@ -114,6 +125,4 @@ def attach_maps(shard: Shard, global_model) -> Shard:
                 jac_map[lo:lo + stp.nrec] = gtp.jac_slices[s][0] + R
         for sp_pair, gp_pair in zip(stp.hess_pairs, gtp.hess_pairs):
             hess_map[sp_pair.start:sp_pair.start + stp.nrec] = gp_pair.start + R
-    shard.var_map, shard.owned_vars = var_map, owned
-    shard.row_map, shard.jac_map, shard.hess_map = row_map, jac_map, hess_map
-    return shard
+    return var_map, owned_mask, row_map, jac_map, hess_map

@@ -21,18 +21,42 @@ import numpy as np
 from .opf import mpopf_model, opf_model
 from .synth import demand_curve, pglib_shaped
 
-WORKLOADS = ("case14", "case1354", "case2000", "case13659", "mp96_case1354")
+WORKLOADS = ("case14", "case1354", "case2000", "case13659", "mp96_case1354", "n1_case2000")
+SHARDED = ("mp", "n1")  # batched configs: one instance sharded over the ranks
 
 
-def build_workload(name: str, lower_to_gpu: bool = True, seed: int = 1):
+def _parse(name: str):
+    head, base = name.split("_", 1)
+    return head, base
+
+
+def n1_contingencies(case, K: int):
+    """Branches 0..K-1 outaged one at a time."""
+    return list(range(min(K, len([b for b in case.branches if b.status == 1]))))
+
+
+def build_workload(name: str, lower_to_gpu: bool = True, seed: int = 1, rank: int = 0, world: int = 1):
+    """Model for a benchmark config; batched configs return rank's shard."""
     if name in ("case14", "case1354", "case2000", "case13659"):
         case = pglib_shaped(name, seed=seed)
         return opf_model(case, form="polar", lower_to_gpu=lower_to_gpu)[0]
-    if name.startswith("mp"):
-        T = int(name[2:].split("_")[0])
-        case = pglib_shaped(name.split("_", 1)[1], seed=seed)
-        return mpopf_model(case, demand_curve(T), corrective_action_ratio=0.25, form="polar",
-                           lower_to_gpu=lower_to_gpu)[0]
+    head, base = _parse(name)
+    case = pglib_shaped(base, seed=seed)
+    if head.startswith("mp"):
+        T = int(head[2:])
+        if world == 1:
+            return mpopf_model(case, demand_curve(T), corrective_action_ratio=0.25, form="polar",
+                               lower_to_gpu=lower_to_gpu)[0]
+        from .sharding import mpopf_shard
+
+        return mpopf_shard(case, demand_curve(T), rank, world, 0.25, lower_to_gpu=lower_to_gpu).model
+    if head.startswith("n1"):
+        K = int(head[2:]) if len(head) > 2 else 1024
+        from .scopf import instance_windows, scopf_model
+
+        cont = n1_contingencies(case, K)
+        owned = instance_windows(len(cont) + 1, world)[rank] if world > 1 else None
+        return scopf_model(case, cont, owned=owned, lower_to_gpu=lower_to_gpu)[0]
     raise KeyError(name)
 
 

@@ -100,3 +100,43 @@ def test_compressed_hessian_at_scale():
     r, cc, smap = O.compress(model.plan.hess_rows, model.plan.hess_cols)
     assert bitwise_equal(hp.rows, r) and bitwise_equal(hp.cols, cc)
     assert bitwise_equal(hp.sum_values(H), O.sum_values(smap, r.size, H))
+
+
+def test_scopf_batch_gpu_parity():
+    from paper_2510_12897_b200.scopf import scopf_model
+    from paper_2510_12897_b200.synth import evaluation_point, synthetic_case
+
+    case = synthetic_case(60, 12, 90, seed=13)
+    model = scopf_model(case, list(range(0, 60, 3)))[0]
+    x, y, w = evaluation_point(model, 5)
+    got = _gpu_set(model, x, y, w)
+    O.use_trig(crtrig.TRIG)
+    try:
+        cr = O.eval_set(model.plan, x, y, w)
+    finally:
+        O.use_trig(None)
+    ref = O.eval_set(model.plan, x, y, w)
+    for a, o, r in zip(got, cr, ref):
+        assert bitwise_equal(a, o)
+        bad = strict_violations(a, r)
+        assert bitwise_equal(a[bad], o[bad])
+
+
+def test_period_shards_on_gpu_reassemble_global():
+    from paper_2510_12897_b200 import mpopf_model
+    from paper_2510_12897_b200.sharding import attach_maps, mpopf_shard
+    from paper_2510_12897_b200.synth import demand_curve, evaluation_point, synthetic_case
+
+    case = synthetic_case(60, 12, 90, seed=21)
+    curve = demand_curve(8)
+    gm = mpopf_model(case, curve, 0.25)[0]
+    x, y, w = evaluation_point(gm, 6)
+    gc, gJ, gH = _gpu_set(gm, x, y, w)
+    c = np.full(gm.ncon, np.nan)
+    J = np.full(gm.plan.n_jac_slots, np.nan)
+    H = np.full(gm.plan.n_hess_slots, np.nan)
+    for r in range(3):
+        sh = attach_maps(mpopf_shard(case, curve, r, 3), gm)
+        sc, sJ, sH = _gpu_set(sh.model, x[sh.var_map], y[sh.row_map], w)
+        c[sh.row_map], J[sh.jac_map], H[sh.hess_map] = sc, sJ, sH
+    assert bitwise_equal(c, gc) and bitwise_equal(J, gJ) and bitwise_equal(H, gH)
