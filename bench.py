@@ -185,7 +185,7 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.workload.startswith(("mp", "n1")) else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.workload, "sets_per_step": cores},
         "cpu_baseline": {"value": value, "unit": "sets/s", "cores": cores, "kind": "port",
                          "sample": f"{sets} sets ({cores} processes x {args.steps} steps) of "
@@ -383,7 +383,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {
             "workload": args.workload, "sets_per_step": S, "form": "polar",
             "nvar": summ["nvar"], "ncon": summ["ncon"], "jac_slots": summ["jac_slots"],
