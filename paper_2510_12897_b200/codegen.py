@@ -612,6 +612,16 @@ class PatternCode:
             out.append("    }")
             out.append("  }")
         out.append("}")
+        # single-variable, field-free patterns also get a value function of the
+        # gathered value itself (pre-resolved fold lanes, see device._row_layout)
+        self.valx_ok = k == 1 and self.nf == 0 and not self.has_checks
+        if self.valx_ok:
+            gx = Gen()
+            vx = self._values(gx, {"field": {}, "var": [Sym("x0")]})
+            out.append(f"__device__ __forceinline__ double exa_valx_{pid}(const double x0) {{")
+            out.extend(gx.lines)
+            out.append(f"  return {R(vx[-1])};")
+            out.append("}")
         # records per thread: light patterns amortise per-thread overheads and
         # overlap several records' loads; heavy ones keep one record per thread
         n_ops = len(g.lines)

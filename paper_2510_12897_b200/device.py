@@ -128,7 +128,10 @@ def collect_patterns(plan):
     return pcodes, term_pid
 
 
-def _row_layout(base_tp, base_dev, augs, dev_index):
+PRERESOLVE = 1 << 30  # fold slot flag: .y holds the global variable id, not a record
+
+
+def _row_layout(base_tp, base_dev, augs, dev_index, valx=None):
     """Contributions per base row in reference order (base, then augments in
     registration order, records in order).  Returns ``(None, None, slots)`` for
     the warp-fold layout -- rows packed into 32-lane warps, slot =
@@ -138,8 +141,16 @@ def _row_layout(base_tp, base_dev, augs, dev_index):
     lrows, terms_, recs = [], [], []
     for a in augs:
         lrows.append(np.asarray(a.rows, dtype=np.int64) - base_tp.row_offset)
-        terms_.append(np.full(a.nrec, dev_index[id(a)], dtype=np.int64))
-        recs.append(np.arange(a.nrec, dtype=np.int64))
+        t_a = dev_index[id(a)]
+        if valx is not None and t_a in valx:
+            # single-variable, field-free augment (pg, -p, ...): pre-resolve the
+            # gathered variable so the fold lane needs one dependent load, not two
+            gid = a.slot_blocks[0].offset + np.asarray(a.table.indices[a.tape.slots[0][1]], dtype=np.int64)
+            terms_.append(np.full(a.nrec, t_a | PRERESOLVE, dtype=np.int64))
+            recs.append(gid)
+        else:
+            terms_.append(np.full(a.nrec, t_a, dtype=np.int64))
+            recs.append(np.arange(a.nrec, dtype=np.int64))
     lrows = np.concatenate(lrows) if lrows else np.zeros(0, np.int64)
     terms_ = np.concatenate(terms_) if terms_ else np.zeros(0, np.int64)
     recs = np.concatenate(recs) if recs else np.zeros(0, np.int64)
@@ -149,6 +160,8 @@ def _row_layout(base_tp, base_dev, augs, dev_index):
     np.cumsum(counts, out=ptr[1:])
     ent = np.stack([terms_[order], recs[order]], axis=1)
     if (counts.size and counts.max() + 1 > 32) or len(dev_index) >= 2**16:
+        if valx:
+            return _row_layout(base_tp, base_dev, augs, dev_index, None)
         return _i32(ptr, "row CSR"), _i32(ent, "row CSR entries"), None
     # greedy packing of rows (1 + augments each) into 32-lane warps
     length = (counts + 1).astype(np.int64)
@@ -172,7 +185,7 @@ def _row_layout(base_tp, base_dev, augs, dev_index):
         row_of = lrows[order]
         pos = np.arange(ent.shape[0]) - ptr[row_of] + 1  # 1-based position within the row
         at = base_slot[row_of] + pos
-        slots[at, 0] = ent[:, 0] | (pos << 16)
+        slots[at, 0] = ent[:, 0] | (pos << 16)  # PRERESOLVE (bit 30) survives the OR
         slots[at, 1] = ent[:, 1]
     return None, None, _i32(slots, "fold slots")
 
@@ -197,6 +210,7 @@ class HostLayout:
             if tp.kind == "augment":
                 targets.setdefault(tp.target_index, []).append(tp)
         self._members: dict = {}
+        self.specialised_ok = len(terms) <= META_CONST_MAX_TERMS
 
         f64 = _Blob(np.float64)
         i32 = _Blob(np.int32)
@@ -227,7 +241,9 @@ class HostLayout:
             if tp.kind == "constraint" and tp.block_index in targets:
                 augs = targets[tp.block_index]
                 self._members[t] = [t] + [dev_index[id(a)] for a in augs]
-                ptr, ent, slots = _row_layout(tp, t, augs, dev_index)
+                valx = {dev_index[id(a)] for a in augs
+                        if self.patterns[self.term_pid[dev_index[id(a)]]].valx_ok} if self.specialised_ok else None
+                ptr, ent, slots = _row_layout(tp, t, augs, dev_index, valx)
                 if slots is not None:  # int2 entries: ALIGN keeps offsets 8-byte aligned
                     d["row_ent_off"] = i32.add(slots)
                     self.fold_slots[t] = slots.shape[0]

@@ -122,8 +122,8 @@ __device__ __forceinline__ void exa_rowfold(const ExaTerm& T, int slot, const Ex
   const int2 e = __ldg(reinterpret_cast<const int2*>(T.row_ent) + slot);
   EXA_GRID_WAIT();
   const bool pad = e.x < 0;
-  const int p = pad ? 0 : (e.x >> 16);
-  const double v = pad ? 0.0 : val(e.x & 0xffff, e.y);
+  const int p = pad ? 0 : ((e.x >> 16) & 0x3fff);
+  const double v = pad ? 0.0 : val(e.x & (0xffff | (1 << 30)), e.y);
   double acc = (p == 0) ? 0.0 + v : v;
   const unsigned pmax = __reduce_max_sync(0xffffffffu, (unsigned)p);
   for (unsigned s = 1; s <= pmax; ++s) {
@@ -235,9 +235,13 @@ def _specialised_kernels(layout) -> str:
         out.append("\n".join(lines))
     # per augment-target block: value of any contributing (term, record)
     for t, members in layout.row_members().items():
-        cases = "\n".join(
-            f"      case {u}: {{ ExaTerm U; exa_init_T{u}(U, A); return exa_val_{layout.term_pid[u]}(U, rec, A, exa_rank(U, A)); }}"
-            for u in members)
+        lines_c = []
+        for u in members:
+            pc = layout.patterns[layout.term_pid[u]]
+            lines_c.append(f"      case {u}: {{ ExaTerm U; exa_init_T{u}(U, A); return exa_val_{layout.term_pid[u]}(U, rec, A, exa_rank(U, A)); }}")
+            if pc.valx_ok:  # pre-resolved slot: rec is the global variable id
+                lines_c.append(f"      case {u | (1 << 30)}: return exa_valx_{layout.term_pid[u]}(__ldg(A.x + rec));")
+        cases = "\n".join(lines_c)
         out.append(f"""__device__ __forceinline__ double exa_rowval_T{t}(int term, int rec, const ExaArgs& A) {{
   switch (term) {{
 {cases}
