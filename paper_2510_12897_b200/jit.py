@@ -25,7 +25,7 @@ CSRC = Path(__file__).resolve().parent / "csrc"
 CACHE_DIR = Path(os.environ.get("EXA_JIT_CACHE", Path(__file__).resolve().parent / "_jit"))
 NVRTC_OPTIONS = ("-arch=sm_100a", "--fmad=false", "-default-device", "-std=c++17", "-lineinfo",
                  "--extra-device-vectorization")
-THREADS = int(os.environ.get("EXA_THREADS", "256"))  # light kernels
+THREADS = int(os.environ.get("EXA_THREADS", "64"))  # CTA size (fused / light kernels)
 THREADS_HEAVY = int(os.environ.get("EXA_THREADS_HEAVY", "128"))  # heavy kernels
 # tuning knobs (experiments only; defaults are the product configuration)
 MIN_BLOCKS = int(os.environ.get("EXA_MINB", "0"))
