@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define EXA_ABI_VERSION 2
+#define EXA_ABI_VERSION 3
 #define EXA_MAXF 16
 #define EXA_MAXI 16
 #define EXA_MAXK 16
@@ -110,6 +110,13 @@ typedef struct ExaPlanDesc {
   const void* cubin;
   int64_t cubin_size;
   int32_t has_domain_checks;
+  /* persistent kernels: persist[kid] = V > 0 -> the kernel's real CTAs hold V
+     virtual CTAs (threads[kid & 1] threads each) and stride over n_ctas[kid]
+     virtual CTAs; the grid is one wave (occupancy x SM count) */
+  int32_t persist[EXA_NKERN];
+  /* the module was built with programmatic-dependent-launch waits: launch
+     with cudaLaunchAttributeProgrammaticStreamSerialization */
+  int32_t pdl;
 } ExaPlanDesc;
 
 /* ---- build-time: JIT ---------------------------------------------------- */
@@ -150,6 +157,11 @@ int exa_domain_error(ExaPlan* plan, ExaWorkspace* ws, exa_stream_t stream, int64
 
 /* ---- diagnostics -------------------------------------------------------- */
 const char* exa_last_error(void);
+/* Timeline buffer for modules generated with EXA_TRACE=1 (8 int64 words per
+ * warp and virtual CTA: SM id, virtual CTA, clock64 start/end, globaltimer
+ * start/end, 2 unused);
+ * NULL disables.  Process-global; not for production use. */
+int exa_debug_trace(void* device_buffer);
 int exa_device_sincos(const double* x, double* s, double* c, int64_t n, exa_stream_t stream);
 
 #ifdef __cplusplus

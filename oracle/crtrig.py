@@ -35,6 +35,10 @@ def _load():
         lib = C.CDLL(str(SO))
         lib.cr_sincos_vec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
         lib.cr_sincos_vec.restype = None
+        lib.cr_sincos_fast_vec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+        lib.cr_sincos_fast_vec.restype = None
+        lib.cr_sincos_slow_vec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+        lib.cr_sincos_slow_vec.restype = None
         _lib = lib
     return _lib
 
@@ -44,6 +48,23 @@ def sincos(x):
     s = np.empty_like(x)
     c = np.empty_like(x)
     _load().cr_sincos_vec(x.ctypes.data, s.ctypes.data, c.ctypes.data, x.size)
+    return s, c
+
+
+def sincos_fast(x):
+    """Ziv fast path alone (|x| <= pi/4): (s, c, ok)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    s, c = np.empty_like(x), np.empty_like(x)
+    ok = np.empty(x.shape, dtype=np.int32)
+    _load().cr_sincos_fast_vec(x.ctypes.data, s.ctypes.data, c.ctypes.data, ok.ctypes.data, x.size)
+    return s, c, ok.astype(bool)
+
+
+def sincos_slow(x):
+    """Double-double slow path alone (|x| <= pi/4)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    s, c = np.empty_like(x), np.empty_like(x)
+    _load().cr_sincos_slow_vec(x.ctypes.data, s.ctypes.data, c.ctypes.data, x.size)
     return s, c
 
 

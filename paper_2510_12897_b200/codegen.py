@@ -32,6 +32,7 @@ Only exact rewrites are applied (x*1 -> x, x*-1 -> -x, x/1 -> x, x-(+0) -> x);
 from __future__ import annotations
 
 import math
+import re
 import os
 
 import numpy as np
@@ -570,7 +571,10 @@ class PatternCode:
         # loads (including the Hessian weight) are issued before the first
         # store, and outputs are __restrict__, so several records per thread
         # (light patterns) overlap their memory latency.
-        out.append(f"template <int MODE>\n__device__ __forceinline__ void exa_term_{pid}(const ExaTerm& T, int r, const ExaArgs& A, int rank) {{")
+        # ``ro`` (default r): record index of the OUTPUT slots and the Hessian
+        # weight, when the term's fields are read from a permuted copy (row buckets)
+        out.append(f"template <int MODE>\n__device__ __forceinline__ void exa_term_{pid}(const ExaTerm& T, int r, const ExaArgs& A, int rank, int ro = -1) {{")
+        out.append("  const int o = ro < 0 ? r : ro;")
         out.append("  double* __restrict__ Cout = A.c;")
         out.append("  double* __restrict__ Jout = A.J;")
         out.append("  double* __restrict__ Hout = A.H;")
@@ -579,23 +583,23 @@ class PatternCode:
         out.extend(pre[pre_wait:])
         if k:
             out.append("  const double wgt = !(MODE & EXA_M_HESS) ? 0.0 : (T.kind == EXA_OBJ) ? A.w"
-                       " : __ldg(A.y + (T.rows ? __ldg(T.rows + r) : T.row_offset + r));")
+                       " : __ldg(A.y + (T.rows ? __ldg(T.rows + o) : T.row_offset + o));")
         out.extend(value_lines)
         out.append("  if (MODE & (EXA_M_CONS | EXA_M_OBJV)) {")
         out.append(f"    const double root = {R(value_root)};")
-        out.append("    if ((MODE & EXA_M_CONS) && T.cons_direct) Cout[T.row_offset + r] = 0.0 + root;")
-        out.append("    if ((MODE & EXA_M_OBJV) && T.kind == EXA_OBJ) A.V[T.scr0 + r] = root;")
+        out.append("    if ((MODE & EXA_M_CONS) && T.cons_direct) Cout[T.row_offset + o] = 0.0 + root;")
+        out.append("    if ((MODE & EXA_M_OBJV) && T.kind == EXA_OBJ) A.V[T.scr0 + o] = root;")
         out.append("  }")
         if k:
             out.append("  if (MODE & (EXA_M_JAC | EXA_M_GRAD | EXA_M_HESS)) {")
             out.extend("  " + l for l in body_grad)
             out.append("    if ((MODE & EXA_M_JAC) && T.kind != EXA_OBJ) {")
             for s in range(k):
-                out.append(f"      Jout[T.jac0 + {s}LL * T.nrec + r] = {R(grads[s])};")
+                out.append(f"      Jout[T.jac0 + {s}LL * T.nrec + o] = {R(grads[s])};")
             out.append("    }")
             out.append("    if ((MODE & EXA_M_GRAD) && T.kind == EXA_OBJ) {")
             for s in range(k):
-                out.append(f"      A.G[T.scr0 + {s}LL * T.nrec + r] = {R(grads[s])};")
+                out.append(f"      A.G[T.scr0 + {s}LL * T.nrec + o] = {R(grads[s])};")
             out.append("    }")
             out.append("    if (MODE & EXA_M_HESS) {")
             out.extend("    " + l for l in body_hess)
@@ -607,7 +611,7 @@ class PatternCode:
                     bi, bj = self.slot_struct[i][0], self.slot_struct[j][0]
                     if i != j and bi == bj:
                         expr = f"(c{i} == c{j} ? {expr} * 2.0 : {expr})"
-                    out.append(f"      Hout[T.hess0 + {pair}LL * T.nrec + r] = wgt * {expr};")
+                    out.append(f"      Hout[T.hess0 + {pair}LL * T.nrec + o] = wgt * {expr};")
                     pair += 1
             out.append("    }")
             out.append("  }")
@@ -622,129 +626,133 @@ class PatternCode:
             out.extend(gx.lines)
             out.append(f"  return {R(vx[-1])};")
             out.append("}")
+            # ... and its Jacobian / weighted Hessian entry (row buckets write the
+            # augment's J/H slots from the row thread), same replay as above
+            gx = Gen()
+            vx = self._values(gx, {"field": {}, "var": [Sym("x0")]})
+            gx.deriv = _DERIV_ZERO_ELISION
+            adjx = self._adjoints(gx, vx)
+            gradx = self._slot_sums(gx, adjx)
+            tx = self._tangents(gx, vx, 0)
+            colx = self._slot_sums(gx, self._adjoint_tangents(gx, vx, adjx, tx))
+            out.append(f"__device__ __forceinline__ void exa_termx_{pid}(const double x0, const double wgt, double& jv, double& hv) {{")
+            out.extend(gx.lines)
+            out.append(f"  jv = {R(gradx[0])};")
+            out.append(f"  hv = wgt * {R(colx[0])};")
+            out.append("}")
         # records per thread: light patterns amortise per-thread overheads and
         # overlap several records' loads; heavy ones keep one record per thread
         n_ops = len(g.lines)
         heavy = bool(g.sincos) or any(ins[0] in ("exp", "log", "pow") for ins in self.instr) or k > 2
         self.rpt = int(os.environ.get("EXA_RPT_LIGHT", "1")) if (not heavy and n_ops <= 40) else 1
         self.heavy = heavy
+        self.uses_sincos = bool(g.sincos)
         return "\n".join(out)
 
     def group_source(self, gid: int, members: list) -> str:
-        """One thread evaluates record r of several terms of this pattern.
-
-        ``members[m] = {"cols": [group column id per index column],
-        "blocks": [group block id per slot]}``: index columns with the same
-        content are loaded once, variables with the same (block, column) are
-        gathered once, and every identical sub-expression -- in OPF the 4 branch
-        flow blocks share vm_f, vm_t, va_f, va_t and sin/cos(va_f - va_t) --
-        is computed once (the generator's CSE), while each member's outputs keep
-        the reference's per-term operation order."""
-        self.instr = self.tape_norm()
-        k = self.k
-        M = len(members)
-        g = Gen()
-        pre, post = [], []
-        u_src: dict = {}
-        for m, mem in enumerate(members):
-            for c, u in enumerate(mem["cols"]):
-                u_src.setdefault(u, (m, c))
-        for u, (m, c) in sorted(u_src.items()):
-            pre.append(f"  const int i{u} = __ldg(T{m}.ix[{c}] + r);")
-        fsyms = []
-        for m in range(M):
-            d = {}
-            for fi, fname in enumerate(self.tape.field_names):
-                pre.append(f"  const double f{m}_{fi} = __ldg(T{m}.f[{fi}] + r);")
-                d[fname] = Sym(f"f{m}_{fi}")
-            fsyms.append(d)
-        xkey: dict = {}
-        vsyms, cnames = [], []
-        for m, mem in enumerate(members):
-            vs, cn = [], []
-            for s_, (_, ic) in enumerate(self.slot_struct):
-                key = (mem["blocks"][s_], mem["cols"][ic])
-                if key not in xkey:
-                    n = len(xkey)
-                    xkey[key] = n
-                    post.append(f"  const int cg{n} = T{m}.voff[{s_}] + i{mem['cols'][ic]};")
-                    post.append(f"  const double xg{n} = __ldg(A.x + cg{n});")
-                vs.append(Sym(f"xg{xkey[key]}"))
-                cn.append(f"cg{xkey[key]}")
-            vsyms.append(vs)
-            cnames.append(cn)
-        if k:
-            for m in range(M):
-                post.append(f"  const double wgt{m} = !(MODE & EXA_M_HESS) ? 0.0 : (T{m}.kind == EXA_OBJ) ? A.w"
-                            f" : __ldg(A.y + (T{m}.rows ? __ldg(T{m}.rows + r) : T{m}.row_offset + r));")
-        R = Gen.r
-        # Stores are emitted as soon as their value is final (cons after the
-        # value pass, J after the adjoint sweep, each Hessian column after its
-        # seed's sweep) so that the LSU drains while the next sweep computes.
-        for m in range(M):
-            T = f"T{m}"
-            g.lines.append(f"  rank = rank{m};")
-            g.deriv = False
-            v = self._values(g, {"field": fsyms[m], "var": vsyms[m]})
-            root = v[-1]
-            g.lines.append(f"  if ((MODE & EXA_M_CONS) && {T}.cons_direct) Cout[{T}.row_offset + r] = 0.0 + {R(root)};")
-            g.lines.append(f"  if ((MODE & EXA_M_OBJV) && {T}.kind == EXA_OBJ) A.V[{T}.scr0 + r] = {R(root)};")
-            if not k:
-                continue
-            g.deriv = _DERIV_ZERO_ELISION
-            adj = self._adjoints(g, v)
-            grads = self._slot_sums(g, adj)
-            for s_ in range(k):
-                g.lines.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
-                g.lines.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
-            for seed in range(k):
-                t = self._tangents(g, v, seed)
-                col = self._slot_sums(g, self._adjoint_tangents(g, v, adj, t))
-                j = seed
-                for i in range(j, k):
-                    expr = R(col[i])
-                    if i != j and self.slot_struct[i][0] == self.slot_struct[j][0]:
-                        expr = f"({cnames[m][i]} == {cnames[m][j]} ? {expr} * 2.0 : {expr})"
-                    pair = i * (i + 1) // 2 + j
-                    g.lines.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
-        res = []
-        args = ", ".join(f"const ExaTerm& T{m}" for m in range(M))
-        ranks = ", ".join(f"int rank{m}" for m in range(M))
-        out = [f"template <int MODE>\n__device__ __forceinline__ void exa_grp_{gid}({args}, int r, const ExaArgs& A, {ranks}) {{",
-               "  double* __restrict__ Cout = A.c;", "  double* __restrict__ Jout = A.J;",
-               "  double* __restrict__ Hout = A.H;", "  int rank = rank0;"]
-        out.extend(pre)
-        out.append("  EXA_GRID_WAIT();")
-        out.extend(post)
-        out.extend(g.lines)
-        for m, (root, grads, by_seed) in enumerate(res):  # (stores already emitted inline)
-            T = f"T{m}"
-            out.append("  if (MODE & (EXA_M_CONS | EXA_M_OBJV)) {")
-            out.append(f"    if ((MODE & EXA_M_CONS) && {T}.cons_direct) Cout[{T}.row_offset + r] = 0.0 + {R(root)};")
-            out.append(f"    if ((MODE & EXA_M_OBJV) && {T}.kind == EXA_OBJ) A.V[{T}.scr0 + r] = {R(root)};")
-            out.append("  }")
-            if not k:
-                continue
-            out.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) {{")
-            for s_ in range(k):
-                out.append(f"    Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
-            out.append("  }")
-            out.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) {{")
-            for s_ in range(k):
-                out.append(f"    A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
-            out.append("  }")
-            out.append("  if (MODE & EXA_M_HESS) {")
-            pair = 0
-            for i in range(k):
-                for j in range(i + 1):
-                    expr = R(by_seed[j][i])
-                    if i != j and self.slot_struct[i][0] == self.slot_struct[j][0]:
-                        expr = f"({cnames[m][i]} == {cnames[m][j]} ? {expr} * 2.0 : {expr})"
-                    out.append(f"    Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
-                    pair += 1
-            out.append("  }")
-        out.append("}")
-        return "\n".join(out)
+        """Group of terms of this one pattern (see :func:`group_source`)."""
+        return group_source(gid, [(self, mem) for mem in members])
 
     def tape_norm(self):
         return list(self.tape.instr)
+
+
+def group_source(gid: int, entries: list) -> str:
+    """One thread evaluates record r of several terms (a *term group*).
+
+    ``entries[m] = (PatternCode, {"cols": [group column id per index column],
+    "blocks": [group block id per slot]})``; members may have different
+    patterns (OPF: the two flow blocks of a branch side plus the thermal and
+    angle-difference terms of the same branches).  Index columns with the same
+    content are loaded once, variables with the same (block, column) are
+    gathered once, and every identical sub-expression -- e.g. sin/cos(va_f -
+    va_t) -- is computed once (the generator's CSE), while each member's
+    outputs keep the reference's per-term operation order."""
+    M = len(entries)
+    g = Gen()
+    pre, post = [], []
+    u_src: dict = {}
+    for m, (pc, mem) in enumerate(entries):
+        pc.instr = pc.tape_norm()
+        for c, u in enumerate(mem["cols"]):
+            u_src.setdefault(u, (m, c))
+    for u, (m, c) in sorted(u_src.items()):
+        pre.append(f"  const int i{u} = __ldg(T{m}.ix[{c}] + r);")
+    fsyms = []
+    for m, (pc, mem) in enumerate(entries):
+        d = {}
+        for fi, fname in enumerate(pc.tape.field_names):
+            pre.append(f"  const double f{m}_{fi} = __ldg(T{m}.f[{fi}] + r);")
+            d[fname] = Sym(f"f{m}_{fi}")
+        fsyms.append(d)
+    xkey: dict = {}
+    vsyms, cnames = [], []
+    for m, (pc, mem) in enumerate(entries):
+        vs, cn = [], []
+        for s_, (_, ic) in enumerate(pc.slot_struct):
+            key = (mem["blocks"][s_], mem["cols"][ic])
+            if key not in xkey:
+                n = len(xkey)
+                xkey[key] = n
+                post.append(f"  const int cg{n} = T{m}.voff[{s_}] + i{mem['cols'][ic]};")
+                post.append(f"  const double xg{n} = __ldg(A.x + cg{n});")
+            vs.append(Sym(f"xg{xkey[key]}"))
+            cn.append(f"cg{xkey[key]}")
+        vsyms.append(vs)
+        cnames.append(cn)
+    for m, (pc, mem) in enumerate(entries):
+        if pc.k:
+            post.append(f"  const double wgt{m} = !(MODE & EXA_M_HESS) ? 0.0 : (T{m}.kind == EXA_OBJ) ? A.w"
+                        f" : __ldg(A.y + (T{m}.rows ? __ldg(T{m}.rows + r) : T{m}.row_offset + r));")
+    R = Gen.r
+    # Stores are emitted as soon as their value is final (cons after the
+    # value pass, J after the adjoint sweep, each Hessian column after its
+    # seed's sweep) so that the LSU drains while the next sweep computes.
+    for m, (pc, mem) in enumerate(entries):
+        k = pc.k
+        T = f"T{m}"
+        g.lines.append(f"  rank = rank{m};")
+        g.deriv = False
+        v = pc._values(g, {"field": fsyms[m], "var": vsyms[m]})
+        root = v[-1]
+        g.lines.append(f"  if ((MODE & EXA_M_CONS) && {T}.cons_direct) Cout[{T}.row_offset + r] = 0.0 + {R(root)};")
+        g.lines.append(f"  if ((MODE & EXA_M_OBJV) && {T}.kind == EXA_OBJ) A.V[{T}.scr0 + r] = {R(root)};")
+        if not k:
+            continue
+        g.deriv = _DERIV_ZERO_ELISION
+        adj = pc._adjoints(g, v)
+        grads = pc._slot_sums(g, adj)
+        for s_ in range(k):
+            g.lines.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
+            g.lines.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
+        for seed in range(k):
+            t = pc._tangents(g, v, seed)
+            col = pc._slot_sums(g, pc._adjoint_tangents(g, v, adj, t))
+            j = seed
+            for i in range(j, k):
+                expr = R(col[i])
+                if i != j and pc.slot_struct[i][0] == pc.slot_struct[j][0]:
+                    expr = f"({cnames[m][i]} == {cnames[m][j]} ? {expr} * 2.0 : {expr})"
+                pair = i * (i + 1) // 2 + j
+                g.lines.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
+    args = ", ".join(f"const ExaTerm& T{m}" for m in range(M))
+    ranks = ", ".join(f"int rank{m}" for m in range(M))
+    out = [f"template <int MODE>\n__device__ __forceinline__ void exa_grp_{gid}({args}, int r, const ExaArgs& A, {ranks}) {{",
+           "  double* __restrict__ Cout = A.c;", "  double* __restrict__ Jout = A.J;",
+           "  double* __restrict__ Hout = A.H;", "  int rank = rank0;"]
+    out.extend(pre)
+    out.append(f"  EXA_TP(0, i{min(u_src)});" if u_src else "  EXA_TP(0, 0.0);")
+    out.append("  EXA_GRID_WAIT();")
+    out.extend(post)
+    if xkey:
+        out.append("  EXA_TP(1, " + " + ".join(f"xg{n}" for n in range(len(xkey))) + ");")
+    # phase stamp 2 after the first sin/cos
+    lines = list(g.lines)
+    for i, ln in enumerate(lines):
+        m_ = re.search(r"exa_sincos\(.*?&(\w+), &(\w+)\)", ln)
+        if m_:
+            lines.insert(i + 1, f"  EXA_TP(2, {m_.group(1)} + {m_.group(2)});")
+            break
+    out.extend(lines)
+    out.append("}")
+    return "\n".join(out)

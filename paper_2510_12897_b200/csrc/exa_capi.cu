@@ -30,6 +30,7 @@ static_assert(sizeof(ExaSegDesc) == sizeof(ExaSeg), "segment layout");
 namespace {
 
 thread_local std::string g_err;
+static long long* g_trace = nullptr;  // exa_debug_trace: timeline buffer for EXA_TRACE modules
 
 int fail(const char* fmt, ...) {
   char buf[1024];
@@ -86,6 +87,8 @@ struct ExaPlan {
   ExaSeg* segs[EXA_NKERN] = {};
   int* cta_seg[EXA_NKERN] = {};
   int n_ctas[EXA_NKERN] = {};
+  int persist[EXA_NKERN] = {};  /* virtual CTAs per real CTA (0 = classic grid) */
+  int grid[EXA_NKERN] = {};     /* real CTAs launched */
   int n_segs_mode[EXA_NKERN] = {};
   int err_base[EXA_NMODES][2] = {};
   int64_t n_vscr = 0, n_gscr = 0;
@@ -219,6 +222,11 @@ extern "C" {
 
 const char* exa_last_error(void) { return g_err.c_str(); }
 
+int exa_debug_trace(void* device_buffer) {
+  g_trace = reinterpret_cast<long long*>(device_buffer);
+  return 0;
+}
+
 void exa_free(void* p) { free(p); }
 
 int exa_nvrtc_version(int* major, int* minor) {
@@ -331,8 +339,10 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
   p->n_jac = d->n_jac;
   p->n_hess = d->n_hess;
   {
-    const char* e = getenv("EXA_PDL");  // programmatic dependent launch: opt-in (no measured gain)
-    p->pdl = (e && e[0] == '1') ? 1 : 0;
+    // programmatic dependent launch only for modules built with the waits;
+    // EXA_PDL=0 in the environment turns it off for experiments
+    const char* e = getenv("EXA_PDL");
+    p->pdl = (d->pdl && !(e && e[0] == '0')) ? 1 : 0;
   }
   p->threads[0] = d->threads[0] > 0 ? d->threads[0] : 128;
   p->threads[1] = d->threads[1] > 0 ? d->threads[1] : 256;
@@ -409,10 +419,23 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
 
   cudaError_t e = cudaLibraryLoadData(&p->lib, d->cubin, nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e != cudaSuccess) return bail(fail("cudaLibraryLoadData: %s", cudaGetErrorString(e)));
+  int n_sm = 0;
+  CU(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, p->device));
   for (int kid = 0; kid < EXA_NKERN; ++kid) {
     e = cudaLibraryGetKernel(&p->kern[kid], p->lib, kKernelNames[kid]);
     if (e != cudaSuccess)
       return bail(fail("cudaLibraryGetKernel(%s): %s", kKernelNames[kid], cudaGetErrorString(e)));
+    const int V = d->persist[kid];
+    p->persist[kid] = V > 0 ? V : 0;
+    p->grid[kid] = p->n_ctas[kid];
+    if (V > 0 && p->n_ctas[kid] > 0) {
+      // one wave: as many real CTAs as can be co-resident, never more than needed
+      int occ = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p->kern[kid], p->threads[kid & 1] * V, 0));
+      if (occ < 1) return bail(fail("kernel %s: zero occupancy", kKernelNames[kid]));
+      const int need = (p->n_ctas[kid] + V - 1) / V;
+      p->grid[kid] = need < occ * n_sm ? need : occ * n_sm;
+    }
   }
   // Constant-memory metadata variant: the module declares exa_terms_c /
   // exa_segs_c; fill them with the term table and all callbacks' segments.
@@ -446,7 +469,8 @@ int exa_plan_info(const ExaPlan* p, int64_t* bytes, int32_t* regs) {
   if (bytes) *bytes = (int64_t)p->bytes;
   if (regs) {
     cudaFuncAttributes a;
-    CU(cudaFuncGetAttributes(&a, (const void*)p->kern[EXA_MODE_SET]));
+    const int kid = p->n_ctas[2 * EXA_MODE_SET] > 0 ? 2 * EXA_MODE_SET : 2 * EXA_MODE_SET + 1;
+    CU(cudaFuncGetAttributes(&a, (const void*)p->kern[kid]));
     *regs = a.numRegs;
   }
   return 0;
@@ -463,8 +487,8 @@ static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStrea
   // previous work on the stream drains; it loads the (immutable) plan data,
   // then waits (griddepcontrol.wait) before touching caller buffers.
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p->n_ctas[kid]);
-  cfg.blockDim = dim3(p->threads[kid & 1]);
+  cfg.gridDim = dim3(p->grid[kid]);
+  cfg.blockDim = dim3(p->threads[kid & 1] * (p->persist[kid] ? p->persist[kid] : 1));
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -480,6 +504,7 @@ static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStrea
 // workspace's aux stream, forked/joined with events (graph-capturable).
 static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaStream_t st) {
   A.err = w->err;
+  A.trace = g_trace;
   A.obj_base = p->err_base[mode][0];
   A.con_base = p->err_base[mode][1];
   A.f64 = p->f64;

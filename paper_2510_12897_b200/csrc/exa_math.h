@@ -33,6 +33,8 @@
 
 #include "exa_sincos_table.h"
 
+#define EXA_SC(j, k) exa_sc_tab[j][k]
+
 typedef struct {
   double hi, lo;
 } exa_dd;
@@ -111,8 +113,8 @@ EXA_FN void exa_sincos_reduced(exa_dd r, exa_dd* s_out, exa_dd* c_out) {
     *c_out = exa_dd_add(exa_dd_make(1.0, 0.0), cm1);
     return;
   }
-  exa_dd S0 = exa_dd_make(sgn * exa_sc_tab[aj][0], sgn * exa_sc_tab[aj][1]);
-  exa_dd C0 = exa_dd_make(exa_sc_tab[aj][2], exa_sc_tab[aj][3]);
+  exa_dd S0 = exa_dd_make(sgn * EXA_SC(aj, 0), sgn * EXA_SC(aj, 1));
+  exa_dd C0 = exa_dd_make(EXA_SC(aj, 2), EXA_SC(aj, 3));
   exa_dd sr = exa_dd_add(S0, exa_dd_add(exa_dd_mul(S0, cm1), exa_dd_mul(C0, sd)));
   exa_dd ms = exa_dd_make(-S0.hi, -S0.lo);
   exa_dd cr = exa_dd_add(C0, exa_dd_add(exa_dd_mul(C0, cm1), exa_dd_mul(ms, sd)));
@@ -155,42 +157,67 @@ EXA_FN int exa_round_decided(double h, double t, double err, double* out) {
   return 0;
 }
 
-/* Fast path for |x| <= pi/4: plain double evaluation with a running error
- * bound; the result is returned only when that bound proves it is the
- * correctly rounded value (Ziv's strategy).  Otherwise 0 -> slow path. */
+/* Fast path for |x| <= pi/4 (Ziv's strategy): the result is returned only
+ * when a rigorous error bound proves it is the correctly rounded value,
+ * otherwise 0 -> double-double slow path.
+ *
+ *   x = j/64 + d (exact), z = d^2 = zh + zl (exact, fma),
+ *   sin d = d + cs,      cs = d*z*P(z)     (|cs| < 2^-23, error ~2^-76)
+ *   cos d = 1 + cm1,     cm1 = -z/2 + z^2*C2(z)
+ *   sin x = S0 + C0 sin d + S0 (cos d - 1)
+ *   cos x = C0 - S0 sin d + C0 (cos d - 1)
+ * with S0, C0 = sin, cos(j/64) as double-doubles.  The three large parts
+ * (S0h, C0h*d, S0h*(-zh/2)) are added with exact two_prod/two_sum; all
+ * smaller parts go into one double.  The bound (~2^-73 absolute) leaves
+ * about one argument in 10^6 to the slow path, so a warp almost never
+ * diverges into it (a slow-path warp is a latency straggler). */
 EXA_FN int exa_sincos_fast(double ax, double* s_out, double* c_out) {
   const double jd = rint(ax * 64.0);
   const double d = ax - jd * 0.015625; /* exact */
-  const double z = d * d;
-  /* sin d = d + d*ps,  ps = z*(-1/6 + z/120 - z^2/5040 + z^3/362880) */
-  const double ps = z * fma(z, fma(z, fma(z, 0x1.71de3a556c734p-19, -0x1.a01a01a01a01ap-13), 0x1.1111111111111p-7),
-                            -0x1.5555555555555p-3);
-  /* cos d - 1 = z*(-1/2 + z/24 - z^2/720 + z^3/40320 - z^4/3628800) */
-  const double cm1 = z * fma(z, fma(z, fma(z, fma(z, -0x1.27e4fb7789f5cp-22, 0x1.a01a01a01a01ap-16),
-                                               -0x1.6c16c16c16c17p-10), 0x1.5555555555555p-5), -0.5);
-  const double sdl = d * ps;
+  const double zh = d * d;
+  const double zl = fma(d, d, -zh);
+  /* P(z) = -1/6 + z/120 - z^2/5040 + z^3/362880 - z^4/39916800 */
+  const double P = fma(zh, fma(zh, fma(zh, fma(zh, -0x1.ae64567f544e4p-26, 0x1.71de3a556c734p-19),
+                                          -0x1.a01a01a01a01ap-13), 0x1.1111111111111p-7),
+                       -0x1.5555555555555p-3);
+  const double cs = (d * zh) * P;
+  /* C2(z) = 1/24 - z/720 + z^2/40320 - z^3/3628800 + z^4/479001600 */
+  const double C2 = fma(zh, fma(zh, fma(zh, fma(zh, 0x1.1eed8eff8d898p-29, -0x1.27e4fb7789f5cp-22),
+                                           0x1.a01a01a01a01ap-16), -0x1.6c16c16c16c17p-10),
+                        0x1.5555555555555p-5);
+  const double z2c = (zh * zh) * C2;
+  const double cml = fma(-0.5, zl, z2c); /* cos d - 1 = -zh/2 + cml */
   const int j = (int)jd;
   double sv, cv;
   if (j == 0) {
-    if (!exa_round_decided(d, sdl, 0x1p-49 * fabs(sdl), &sv)) return 0;
-    if (!exa_round_decided(1.0, cm1, 0x1p-49 * fabs(cm1), &cv)) return 0;
+    /* sin x = d + cs;  cos x = 1 - zh/2 + cml */
+    if (!exa_round_decided(d, cs, 0x1p-50 * fabs(cs), &sv)) return 0;
+    exa_dd c1 = exa_two_sum(1.0, -0.5 * zh);
+    if (!exa_round_decided(c1.hi, c1.lo + cml, 0x1p-48 * fabs(z2c) + 0x1p-104, &cv)) return 0;
   } else {
-    const double S0h = exa_sc_tab[j][0], S0l = exa_sc_tab[j][1];
-    const double C0h = exa_sc_tab[j][2], C0l = exa_sc_tab[j][3];
-    /* sin x = S0 + C0 d + (S0 cm1 + C0 d ps) */
-    exa_dd p = exa_two_prod(C0h, d);
-    exa_dd h = exa_two_sum(S0h, p.hi);
-    const double a1 = S0h * cm1, a2 = C0h * sdl;
-    double t = h.lo + (p.lo + (S0l + (C0l * d + (a1 + a2))));
-    double err = 0x1p-49 * (fabs(a1) + fabs(a2)) + 0x1p-96 * fabs(h.hi);
-    if (!exa_round_decided(h.hi, t, err, &sv)) return 0;
-    /* cos x = C0 - S0 d + (C0 cm1 - S0 d ps) */
-    exa_dd q = exa_two_prod(S0h, d);
-    exa_dd g = exa_two_sum(C0h, -q.hi);
-    const double b1 = C0h * cm1, b2 = S0h * sdl;
-    t = g.lo + (-q.lo + (C0l + (-(S0l * d) + (b1 - b2))));
-    err = 0x1p-49 * (fabs(b1) + fabs(b2)) + 0x1p-96 * fabs(g.hi);
-    if (!exa_round_decided(g.hi, t, err, &cv)) return 0;
+    const double S0h = EXA_SC(j, 0), S0l = EXA_SC(j, 1);
+    const double C0h = EXA_SC(j, 2), C0l = EXA_SC(j, 3);
+    const double hz = -0.5 * zh; /* exact */
+    {
+      exa_dd p = exa_two_prod(C0h, d);
+      exa_dd q = exa_two_prod(S0h, hz);
+      exa_dd h = exa_two_sum(S0h, p.hi);
+      exa_dd h2 = exa_two_sum(h.hi, q.hi);
+      const double small = (C0h * cs + S0h * cml) + ((C0l * d + S0l * hz) + S0l);
+      const double t = (h.lo + h2.lo) + ((p.lo + q.lo) + small);
+      const double err = 0x1p-48 * (fabs(C0h * cs) + fabs(S0h * cml)) + 0x1p-98 * fabs(h2.hi);
+      if (!exa_round_decided(h2.hi, t, err, &sv)) return 0;
+    }
+    {
+      exa_dd p = exa_two_prod(S0h, d);
+      exa_dd q = exa_two_prod(C0h, hz);
+      exa_dd h = exa_two_sum(C0h, -p.hi);
+      exa_dd h2 = exa_two_sum(h.hi, q.hi);
+      const double small = (C0h * cml - S0h * cs) + ((C0l * hz - S0l * d) + C0l);
+      const double t = (h.lo + h2.lo) + ((q.lo - p.lo) + small);
+      const double err = 0x1p-48 * (fabs(S0h * cs) + fabs(C0h * cml)) + 0x1p-98 * fabs(h2.hi);
+      if (!exa_round_decided(h2.hi, t, err, &cv)) return 0;
+    }
   }
   *s_out = sv;
   *c_out = cv;

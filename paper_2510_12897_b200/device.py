@@ -29,17 +29,28 @@ import numpy as np
 from . import _lib
 from .codegen import PatternCode
 from .core import ModelError
-from .jit import THREADS, THREADS_HEAVY, compile_module, module_source
+from .jit import PDL, PERSIST, THREADS, THREADS_HEAVY, compile_module, module_source
 
 ALIGN = 32  # elements: 256 B for fp64, 128 B for int32
 
 KIND = {"objective": 0, "constraint": 1, "augment": 2}
 OP_LEAF, OP_ADD, OP_CONST, OP_ZERO_PLUS, OP_TOTAL_ADD = range(5)
-SEG_TERM, SEG_ROW, SEG_FOLD, SEG_GROUP = 0, 1, 2, 3
+SEG_TERM, SEG_ROW, SEG_FOLD, SEG_GROUP, SEG_BUCKET = 0, 1, 2, 3, 4
+# Row buckets (specialised modules): augment-target rows whose augments are
+# all single-variable and field-free are evaluated one thread per row, rows
+# grouped by contribution count so the count is a compile-time constant.
+BUCKETS = os.environ.get("EXA_BUCKETS", "1") == "1"
+BUCKET_SEL_BITS = 2                    # augment selector in the entry's top bits
+BUCKET_GID_BITS = 29                   # global variable id bits
+BUCKET_MAX_D = 31                      # at most this many augment contributions per row
+BUCKET_WMAX = 8                        # wider rows: one warp per row (in-order shuffle fold)
+BUCKET_MAX_N = 48                      # at most this many distinct counts per block
 
 # Terms of one heavy pattern that share index columns (OPF: the 4 branch-flow
 # blocks) are evaluated by one thread per record (see codegen.group_source).
 GROUP_MAX = int(os.environ.get("EXA_GROUP_MAX", "2"))
+ATTACH = os.environ.get("EXA_ATTACH", "1") == "1"  # light terms join heavy groups
+GROUP_RPT = int(os.environ.get("EXA_GROUP_RPT", "1"))  # records per thread of term groups (ILP)
 
 # Models with at most this many terms get a *specialised* module (metadata
 # compiled in as constants); larger ones (e.g. thousands of per-instance
@@ -190,6 +201,71 @@ def _row_layout(base_tp, base_dev, augs, dev_index, valx=None):
     return None, None, _i32(slots, "fold slots")
 
 
+def _bucket_layout(base_tp, augs, nvar):
+    """Row buckets of an augment-target block (reference order per row: base,
+    then augments in registration order, records in order, autodiff.py:573-580).
+
+    Every augment must be single-variable and field-free (value = f(x[gid])).
+    Rows are grouped by their number of augment contributions d into width
+    classes W (W/2 < d <= W); within a class rows ascend.  Returns
+    ``[(W, rows, ent, rec)]`` with ``rows`` the in-block row ids, ``ent`` a
+    (W, n) array of ``gid | sel << 29`` in reference order (sel = index of the
+    contributing augment in ``augs``) and ``rec`` the contributing augment
+    records (the row thread also writes their Jacobian/Hessian slots in the
+    fused set kernel), -1 past a row's d; or None when the block does not fit
+    the encoding.  Rows with more than BUCKET_WMAX contributions form the
+    class W = 32 (listed first): one warp per row, arrays (n, 32) row-major,
+    lane 0 reserved for the base term."""
+    if len(augs) > (1 << BUCKET_SEL_BITS) or nvar >= (1 << BUCKET_GID_BITS):
+        return None
+    n = base_tp.nrec
+    lrows, ents, recs = [], [], []
+    for sel, a in enumerate(augs):
+        lrows.append(np.asarray(a.rows, dtype=np.int64) - base_tp.row_offset)
+        gid = a.slot_blocks[0].offset + np.asarray(a.table.indices[a.tape.slots[0][1]], dtype=np.int64)
+        ents.append(gid | (sel << BUCKET_GID_BITS))
+        recs.append(np.arange(a.nrec, dtype=np.int64))
+    lrows = np.concatenate(lrows) if lrows else np.zeros(0, np.int64)
+    ents = np.concatenate(ents) if ents else np.zeros(0, np.int64)
+    recs = np.concatenate(recs) if recs else np.zeros(0, np.int64)
+    order = np.argsort(lrows, kind="stable")  # per row: registration order, then record order
+    lrows, ents, recs = lrows[order], ents[order], recs[order]
+    counts = np.bincount(lrows, minlength=n)
+    if counts.size and (counts.max() > BUCKET_MAX_D or np.unique(counts).size > BUCKET_MAX_N):
+        return None
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=ptr[1:])
+    # width classes W = 0, 1, 2, 4, 8, ...: rows with W/2 < d <= W, entries
+    # padded with -1 (skipped), so the code is unrolled once per class
+    width = np.where(counts == 0, 0, 1 << np.ceil(np.log2(np.maximum(counts, 1))).astype(np.int64))
+    out = []
+    # long rows (d > BUCKET_WMAX): one warp per row, lane l > 0 holds entry l-1
+    # (class W = 32, entries laid out row-major so each warp reads 128 B)
+    long_ = width > BUCKET_WMAX
+    if long_.any():
+        rows = np.flatnonzero(long_)
+        ent = np.full((rows.size, 32), -1, dtype=np.int64)
+        rec = np.full((rows.size, 32), -1, dtype=np.int64)
+        for q, rr in enumerate(rows.tolist()):
+            dd = int(counts[rr])
+            ent[q, 1:dd + 1] = ents[ptr[rr]:ptr[rr] + dd]
+            rec[q, 1:dd + 1] = recs[ptr[rr]:ptr[rr] + dd]
+        width = np.where(long_, -1, width)
+        out.append((32, rows, ent, rec))
+    for W in np.unique(width).tolist():
+        if W < 0:
+            continue
+        rows = np.flatnonzero(width == W)
+        ent = np.full((W, rows.size), -1, dtype=np.int64)
+        rec = np.full((W, rows.size), -1, dtype=np.int64)
+        for k in range(W):
+            has = counts[rows] > k
+            ent[k, has] = ents[ptr[rows[has]] + k]
+            rec[k, has] = recs[ptr[rows[has]] + k]
+        out.append((W, rows, ent, rec))
+    return out
+
+
 class HostLayout:
     """Everything the device needs for one plan, built on the host only."""
 
@@ -216,6 +292,7 @@ class HostLayout:
         i32 = _Blob(np.int32)
         descs = []
         self.fold_slots: dict = {}
+        self.buckets: dict = {}
         scr = 0
         self.scr0 = []
         for t, tp in enumerate(terms):
@@ -241,6 +318,26 @@ class HostLayout:
             if tp.kind == "constraint" and tp.block_index in targets:
                 augs = targets[tp.block_index]
                 self._members[t] = [t] + [dev_index[id(a)] for a in augs]
+                bk = None
+                if (BUCKETS and self.specialised_ok and not pcs[self.term_pid[t]].has_checks
+                        and all(pcs[self.term_pid[dev_index[id(a)]]].valx_ok for a in augs)):
+                    bk = _bucket_layout(tp, augs, plan.nvar)
+                if bk is not None:
+                    lst = []
+                    for (dd, rows, ent, rec) in bk:
+                        lst.append({
+                            "d": dd, "n": int(rows.size),
+                            "rows_off": i32.add(_i32(rows, "bucket rows")),
+                            "ent_off": i32.add(_i32(ent.reshape(-1), "bucket entries")) if dd else -1,
+                            "rec_off": i32.add(_i32(rec.reshape(-1), "bucket records")) if dd else -1,
+                            "f_off": [f64.add(np.asarray(tp.reals[nm])[rows]) for nm in tp.tape.field_names],
+                            "ix_off": [i32.add(_i32(np.asarray(tp.table.indices[nm])[rows], f"index column {nm!r}"))
+                                       for nm in tp.tape.index_names],
+                        })
+                    self.buckets[t] = {"buckets": lst, "augs": [dev_index[id(a)] for a in augs],
+                                       "base_k": tp.tape.k}
+                    descs.append(d)
+                    continue
                 valx = {dev_index[id(a)] for a in augs
                         if self.patterns[self.term_pid[dev_index[id(a)]]].valx_ok} if self.specialised_ok else None
                 ptr, ent, slots = _row_layout(tp, t, augs, dev_index, valx)
@@ -269,6 +366,12 @@ class HostLayout:
             if nrec > 0:
                 segs[m].append((t, kind, nrec))
 
+        # set kernel: row threads of bucketed blocks also write the base term's
+        # and their augments' Jacobian/Hessian slots
+        fused_set = set()
+        for t, info in self.buckets.items():
+            fused_set.add(t)
+            fused_set.update(info["augs"])
         for t, tp in enumerate(terms):
             k = tp.tape.k
             chk = pcs[self.term_pid[t]].has_checks
@@ -284,7 +387,7 @@ class HostLayout:
                     seg(_lib.MODE_OBJV, t, SEG_TERM, tp.nrec)
                 continue
             direct = bool(descs[t]["cons_direct"])
-            if k or direct:
+            if (k or direct) and t not in fused_set:
                 seg(_lib.MODE_SET, t, SEG_TERM, tp.nrec)
             if direct:
                 seg(_lib.MODE_CONS, t, SEG_TERM, tp.nrec)
@@ -293,7 +396,12 @@ class HostLayout:
             if k:
                 seg(_lib.MODE_HESS, t, SEG_TERM, tp.nrec)
             if tp.kind == "constraint" and not direct:
-                if t in self.fold_slots:
+                if t in self.buckets:
+                    for bi, bk in enumerate(self.buckets[t]["buckets"]):
+                        nth = bk["n"] * (32 if bk["d"] == 32 else 1)  # long rows: a warp per row
+                        seg(_lib.MODE_SET, t, SEG_BUCKET + 16 * bi, nth)
+                        seg(_lib.MODE_CONS, t, SEG_BUCKET + 16 * bi, nth)
+                elif t in self.fold_slots:
                     seg(_lib.MODE_SET, t, SEG_FOLD, self.fold_slots[t])
                     seg(_lib.MODE_CONS, t, SEG_FOLD, self.fold_slots[t])
                 else:
@@ -310,7 +418,7 @@ class HostLayout:
                 if filt == "light":
                     return not heavy
                 if filt == "fold":
-                    return kind in (SEG_FOLD, SEG_ROW)
+                    return (kind & 15) in (SEG_FOLD, SEG_ROW, SEG_BUCKET)
                 if filt == "aug":
                     return kind == SEG_TERM and terms[t].kind == "augment"
                 if filt == "other":
@@ -336,7 +444,7 @@ class HostLayout:
                     heavy = SPLIT_HEAVY and kind in (SEG_TERM, SEG_GROUP) and pcs[self.term_pid[t]].heavy
                     if heavy != (half == 0):
                         continue
-                    rpt = pcs[self.term_pid[t]].rpt if kind == SEG_TERM else 1
+                    rpt = pcs[self.term_pid[t]].rpt if kind == SEG_TERM else (GROUP_RPT if kind == SEG_GROUP else 1)
                     if kind == SEG_GROUP:  # segment names the group, not the term
                         t = self.group_of[t]
                     lst.append((t, kind, cta, nrec, rpt))
@@ -364,6 +472,9 @@ class HostLayout:
 
         # ---- module source ---------------------------------------------------
         self.specialised = len(terms) <= META_CONST_MAX_TERMS
+        # persistent kernels (specialised modules): PERSIST virtual CTAs per real CTA
+        self.persist = [PERSIST if (self.specialised and self.n_ctas[kid]) else 0 for kid in range(_lib.NKERN)]
+        self.pdl = PDL
         self.source = module_source(self.patterns, meta_const=False,
                                     layout=self if self.specialised else None)
 
@@ -380,8 +491,10 @@ class HostLayout:
                 continue
             key = (self.term_pid[t], tp.nrec, tp.kind, descs[t]["cons_direct"])
             sig.setdefault(key, []).append(t)
+        hashes = {t: [col_hash(tp.table.indices[nm]) for nm in tp.tape.index_names]
+                  for t, tp in enumerate(terms) if tp.nrec}
+        groups = []
         for key, cand in sig.items():
-            hashes = {t: [col_hash(terms[t].table.indices[nm]) for nm in terms[t].tape.index_names] for t in cand}
             free = list(cand)
             while free:
                 t0 = free.pop(0)
@@ -394,20 +507,56 @@ class HostLayout:
                         grp.append(u)
                         cols |= set(hashes[u])
                         free.remove(u)
-                if len(grp) < 2:
+                if len(grp) >= 2:
+                    groups.append(grp)
+        # Light constraint terms over the same records that gather some of the
+        # same variables (OPF: thermal limits and angle differences of the
+        # branches) join the heavy group with which they share most gathers;
+        # their loads and gathers are then shared (fewer random L2 sectors).
+        if ATTACH and groups:
+            def keys(t):
+                tp = terms[t]
+                hs = hashes[t]
+                ss = self.patterns[self.term_pid[t]].slot_struct
+                return {(id(tp.slot_blocks[s_]), hs[ic]) for s_, (_, ic) in enumerate(ss)}
+
+            def attachable(t):
+                tp = terms[t]
+                pc = self.patterns[self.term_pid[t]]
+                return (tp.kind == "constraint" and descs[t]["cons_direct"] and tp.tape.k > 0
+                        and not pc.heavy and not pc.has_checks and tp.nrec > 0)
+
+            in_grp = {t for grp in groups for t in grp}
+            gkeys = [set().union(*(keys(t) for t in grp)) for grp in groups]
+            for t in range(len(terms)):
+                if t in in_grp or not attachable(t):
                     continue
-                uid: dict = {}
-                bid: dict = {}
-                members = []
-                for t in grp:
-                    members.append({
-                        "cols": [uid.setdefault(h, len(uid)) for h in hashes[t]],
-                        "blocks": [bid.setdefault(id(b), len(bid)) for b in terms[t].slot_blocks],
-                    })
-                gi = len(self.groups)
-                self.groups.append((self.term_pid[t0], grp, members))
-                for t in grp:
-                    self.group_of[t] = gi
+                kt = keys(t)
+                best, score = None, 0
+                for gi, grp in enumerate(groups):
+                    t0 = grp[0]
+                    if terms[t0].nrec != terms[t].nrec or terms[t0].kind != "constraint" or not descs[t0]["cons_direct"]:
+                        continue
+                    sc = len(kt & gkeys[gi])
+                    if sc > score or (sc == score and sc and len(grp) < len(groups[best])):
+                        best, score = gi, sc
+                if best is not None:
+                    groups[best].append(t)
+                    gkeys[best] |= kt
+        for grp in groups:
+            t0 = grp[0]
+            uid: dict = {}
+            bid: dict = {}
+            members = []
+            for t in grp:
+                members.append({
+                    "cols": [uid.setdefault(h, len(uid)) for h in hashes[t]],
+                    "blocks": [bid.setdefault(id(b), len(bid)) for b in terms[t].slot_blocks],
+                })
+            gi = len(self.groups)
+            self.groups.append((self.term_pid[t0], grp, members))
+            for t in grp:
+                self.group_of[t] = gi
 
     # accessors used by the specialised-kernel generator (jit.py)
     def term_descs(self):
@@ -446,7 +595,7 @@ class HostLayout:
 
 def host_layout(plan) -> HostLayout:
     lay = getattr(plan, "_exa_layout", None)
-    if lay is None or lay.threads != (THREADS_HEAVY, THREADS):
+    if lay is None or lay.threads != (THREADS_HEAVY, THREADS) or lay.pdl != PDL:
         lay = HostLayout(plan)
         plan._exa_layout = lay
     return lay
@@ -494,7 +643,7 @@ class DevicePlan:
             lst = lay.segs[m]
             arr = (_lib.SegDesc * max(1, len(lst)))()
             for s, (t, kind, cta0, nrec, rpt) in enumerate(lst):
-                arr[s].term, arr[s].kind, arr[s].cta0, arr[s].nrec = t, kind | (rpt << 8), cta0, nrec
+                arr[s].term, arr[s].kind, arr[s].cta0, arr[s].nrec = t, (kind & 15) | (rpt << 8), cta0, nrec
             seg_arrays.append(arr)
 
         desc = _lib.PlanDesc()
@@ -513,6 +662,8 @@ class DevicePlan:
             desc.segs[m] = C.cast(seg_arrays[m], C.POINTER(_lib.SegDesc))
             desc.n_segs[m] = len(lay.segs[m])
             desc.n_ctas[m] = lay.n_ctas[m]
+            desc.persist[m] = lay.persist[m]
+        desc.pdl = int(lay.pdl)
         n_obj, n_con = len(plan.obj_terms), len(plan.con_terms)
         bases = {
             _lib.MODE_SET: (n_con, 0), _lib.MODE_CONS: (0, 0), _lib.MODE_JAC: (0, 0),

@@ -20,17 +20,29 @@ import threading
 from pathlib import Path
 
 from . import _lib
+from .codegen import group_source
 
 CSRC = Path(__file__).resolve().parent / "csrc"
 CACHE_DIR = Path(os.environ.get("EXA_JIT_CACHE", Path(__file__).resolve().parent / "_jit"))
 NVRTC_OPTIONS = ("-arch=sm_100a", "--fmad=false", "-default-device", "-std=c++17", "-lineinfo",
                  "--extra-device-vectorization")
-THREADS = int(os.environ.get("EXA_THREADS", "64"))  # CTA size (fused / light kernels)
+THREADS = int(os.environ.get("EXA_THREADS", "32"))  # CTA size (fused / light kernels)
 THREADS_HEAVY = int(os.environ.get("EXA_THREADS_HEAVY", "128"))  # heavy kernels
 # tuning knobs (experiments only; defaults are the product configuration)
-MIN_BLOCKS = int(os.environ.get("EXA_MINB", "0"))
-SINCOS_IMPL = os.environ.get("EXA_SINCOS_IMPL", "cr")
-PDL = os.environ.get("EXA_PDL", "0") == "1"  # must match the library's launch attribute  # "cuda" = libdevice sincos, NOT parity-exact
+MIN_BLOCKS = int(os.environ.get("EXA_MINB", str(1024 // THREADS)))  # 1024 threads/SM -> <= 64 regs
+SINCOS_IMPL = os.environ.get("EXA_SINCOS_IMPL", "cr")  # "cuda" = libdevice sincos, NOT parity-exact
+# Persistent specialised kernels (experiment, off): each real CTA runs PERSIST
+# virtual CTAs of THREADS threads side by side and strides over the model's
+# virtual CTAs.  Measured slower than one CTA per virtual CTA (static
+# assignment cannot balance the long flow CTAs).
+PERSIST = int(os.environ.get("EXA_PERSIST", "0"))
+TRACE = os.environ.get("EXA_TRACE", "0") == "1"  # per-warp timeline (diagnostics builds)
+# Programmatic dependent launch: a CTA releases the next grid once its work is
+# issued; the next grid's CTAs load their (immutable) plan data before
+# griddepcontrol.wait, so back-to-back sets overlap one's drain with the next's
+# launch and first DRAM round trip (case13659: 8.8 -> 8.3 us per set).  The
+# library sets the launch attribute only for modules built with the waits.
+PDL = os.environ.get("EXA_PDL", "1") == "1"
 
 _lock = threading.Lock()
 _mem_cache: dict = {}
@@ -72,6 +84,37 @@ __device__ __forceinline__ void exa_report(const ExaArgs& A, int rank, int instr
 #else
 #define EXA_GRID_WAIT() do {} while (0)
 #define EXA_GRID_RELEASE() do {} while (0)
+#endif
+// diagnostics (EXA_TRACE=1 builds only): per warp and virtual CTA, 12 words
+// (SM id, virtual CTA, clock64 start/end, globaltimer start/end, 4 phase
+// stamps of lane 0 (clock64, 0 = not reached), 2 unused) into A.trace
+#if EXA_TRACE
+__device__ __forceinline__ long long exa_gtimer() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
+__shared__ long long exa_tp_s[EXA_TRACE_NT][4];
+// phase stamp k once `dep` is available (the asm input waits on its scoreboard)
+#define EXA_TP(k, dep)                                                          \
+  do {                                                                          \
+    long long t_;                                                               \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_) : "d"((double)(dep)));     \
+    exa_tp_s[threadIdx.x][k] = t_;                                              \
+  } while (0)
+#define EXA_TRACE_BEGIN() const long long exa_c0_ = clock64(), exa_g0_ = exa_gtimer(); \
+  exa_tp_s[threadIdx.x][0] = exa_tp_s[threadIdx.x][1] = exa_tp_s[threadIdx.x][2] = exa_tp_s[threadIdx.x][3] = 0
+#define EXA_TRACE_END(b, tid, nthreads)                                                       \
+  do {                                                                                      \
+    __syncwarp();                                                                           \
+    if (A.trace && ((tid) & 31) == 0) {                                                     \
+      unsigned smid; asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                      \
+      long long* tr_ = A.trace + 12LL * ((long long)(b) * ((nthreads) / 32) + (tid) / 32);  \
+      tr_[0] = smid; tr_[1] = (b); tr_[2] = exa_c0_; tr_[3] = clock64();                    \
+      tr_[4] = exa_g0_; tr_[5] = exa_gtimer();                                              \
+      for (int k_ = 0; k_ < 4; ++k_) tr_[6 + k_] = exa_tp_s[threadIdx.x][k_];               \
+    }                                                                                       \
+  } while (0)
+#else
+#define EXA_TRACE_BEGIN() do {} while (0)
+#define EXA_TRACE_END(b, tid, nthreads) do {} while (0)
+#define EXA_TP(k, dep) do {} while (0)
 #endif
 """
 
@@ -181,8 +224,8 @@ __device__ __forceinline__ void exa_kernel_body(const ExaTerm* __restrict__ term
 """
 
 _ENTRIES = r"""
-#define EXA_ENTRY(NAME, MODE, BOUNDS)                                                          \
-  extern "C" __global__ void __launch_bounds__(BOUNDS) NAME(                                  \
+#define EXA_ENTRY(NAME, MODE, ...)                                                             \
+  extern "C" __global__ void __launch_bounds__(__VA_ARGS__) NAME(                             \
       const ExaTerm* __restrict__ terms, const ExaSeg* __restrict__ segs,                     \
       const int* __restrict__ cta_seg, ExaArgs A) {                                           \
     EXA_GRID_RELEASE();                                                                        \
@@ -248,51 +291,220 @@ def _specialised_kernels(layout) -> str:
       default: return 0.0;
   }}
 }}""")
+    # row buckets: value of one pre-resolved augment entry (gid | sel << 29)
+    # given its gathered variable, and (set kernel) its J/H slot stores.  The
+    # last augment is the default case, so every path is branch-free selects.
+    for t, info in getattr(layout, "buckets", {}).items():
+        augs = info["augs"]
+        cases = "\n".join(f"    case {sel}: return exa_valx_{layout.term_pid[u]}(xv);"
+                           for sel, u in enumerate(augs[:-1]))
+        last = f"    default: return exa_valx_{layout.term_pid[augs[-1]]}(xv);"
+        out.append(f"""__device__ __forceinline__ double exa_bkval_T{t}(const int e, const double xv) {{
+  switch ((unsigned)e >> 29) {{
+{cases}
+{last}
+  }}
+}}""")
+        descs = layout.term_descs()
+        oc = []
+        for sel, u in enumerate(augs):
+            lab = f"    case {sel}:" if sel < len(augs) - 1 else "    default:"
+            oc.append(f"{lab} exa_termx_{layout.term_pid[u]}(xv, w, jv, hv); j0 = {descs[u]['jac0']}LL;"
+                      f" h0 = {descs[u]['hess0']}LL; break;")
+        ocases = "\n".join(oc)
+        out.append(f"""__device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, const double w, const int rec, const ExaArgs& A) {{
+  double jv, hv;
+  long long j0, h0;
+  switch ((unsigned)e >> 29) {{
+{ocases}
+  }}
+  double* __restrict__ Jout = A.J;  // restrict: later gathers may be hoisted above these stores
+  double* __restrict__ Hout = A.H;
+  Jout[j0 + rec] = jv;
+  Hout[h0 + rec] = hv;
+}}""")
     for gid, (pid, grp, members) in enumerate(getattr(layout, "groups", [])):
-        out.append(layout.patterns[pid].group_source(gid, members))
+        out.append(group_source(gid, [(layout.patterns[layout.term_pid[u]], mem) for u, mem in zip(grp, members)]))
     for m, name in enumerate(KERNEL_NAMES):
-        m_ = m
         for half, suffix in ((0, "_h"), (1, "_l")):
-            kid = 2 * m + half
-            threads = layout.threads[half]
-            body = [f"extern \"C\" __global__ void __launch_bounds__(@BOUNDS_{'H' if half == 0 else 'L'}@) {name}{suffix}(",
-                    "    const ExaTerm* __restrict__ terms, const ExaSeg* __restrict__ segs,",
-                    "    const int* __restrict__ cta_seg, ExaArgs A) {",
-                    "  EXA_GRID_RELEASE();",
-                    "  const int b = (int)blockIdx.x;"]
-            for (t, kind, cta0, nrec, rpt) in layout.mode_segments(kid):
-                n_cta = (nrec + threads * rpt - 1) // (threads * rpt)
-                body.append(f"  if (b < {cta0 + n_cta}) {{")
-                if kind == 3:  # term group: t is the group id
-                    pid, grp, _ = layout.groups[t]
-                    for gm, u in enumerate(grp):
-                        body.append(f"    ExaTerm T{gm}; exa_init_T{u}(T{gm}, A);")
-                    body.append(f"    const int r = (b - {cta0}) * {threads} + (int)threadIdx.x;")
-                    body.append(f"    if (r >= {nrec}) return;")
-                    tl = ", ".join(f"T{gm}" for gm in range(len(grp)))
-                    rl = ", ".join(f"exa_rank(T{gm}, A)" for gm in range(len(grp)))
-                    body.append(f"    exa_grp_{t}<{_MODE_BITS[m_]}>({tl}, r, A, {rl});")
-                    body.append("    return;")
-                    body.append("  }")
-                    continue
-                body.append(f"    ExaTerm T; exa_init_T{t}(T, A);")
-                if kind == 0:
-                    body.append(f"    const int r0 = (b - {cta0}) * {threads * rpt} + (int)threadIdx.x;")
-                    body.append("#pragma unroll")
-                    body.append(f"    for (int q = 0; q < {rpt}; ++q) {{")
-                    body.append(f"      const int r = r0 + q * {threads};")
-                    body.append(f"      if (r < {nrec}) exa_term_{layout.term_pid[t]}<{_MODE_BITS[m]}>(T, r, A, exa_rank(T, A));")
-                    body.append("    }")
-                else:
-                    body.append(f"    const int r = (b - {cta0}) * {threads} + (int)threadIdx.x;")
-                    body.append(f"    if (r >= {nrec}) return;")
-                    fn = "exa_rowfold" if kind == 2 else "exa_row"
-                    body.append(f"    {fn}(T, r, A, [&](int u, int rec) {{ return exa_rowval_T{t}(u, rec, A); }});")
-                body.append("    return;")
-                body.append("  }")
-            body.append("}")
-            out.append("\n".join(body))
+            out.append(_kernel_source(layout, m, half, name + suffix))
     return "\n\n".join(out)
+
+
+def _warp_row_source(layout, t, bi, cta0, n_cta, threads, full):
+    """Long rows of a bucketed block: one warp per row.  Lane 0 evaluates the
+    base term, lane l > 0 augment entry l-1; the row total is folded left to
+    right through the lanes with shuffles -- ((0 + base) + a1) + a2 ... as the
+    reference's slice-add + np.add.at (autodiff.py:573-580)."""
+    bk = layout.buckets[t]["buckets"][bi]
+    n = bk["n"]
+    pid = layout.term_pid[t]
+    L = [f"  if (b < {cta0 + n_cta}) {{", f"    ExaTerm T; exa_init_T{t}(T, A);"]
+    for i, off in enumerate(bk["f_off"]):
+        L.append(f"    T.f[{i}] = A.f64 + {off}LL;")
+    for i, off in enumerate(bk["ix_off"]):
+        L.append(f"    T.ix[{i}] = A.i32 + {off}LL;")
+    L += [f"    const int q = (b - {cta0}) * {threads // 32} + tid / 32;",
+          "    const int lane = tid & 31;",
+          f"    if (q >= {n}) return;  // warp-uniform",
+          f"    const int r = __ldg(A.i32 + {bk['rows_off']}LL + q);",
+          f"    const int e = __ldg(A.i32 + {bk['ent_off']}LL + 32 * q + lane);"]
+    if full:
+        L.append(f"    const int rc = __ldg(A.i32 + {bk['rec_off']}LL + 32 * q + lane);")
+    L.append("    EXA_GRID_WAIT();")
+    if full:
+        L.append("    const double wrow = __ldg(A.y + T.row_offset + r);")
+    L += ["    double v;",
+          "    if (lane == 0) {",
+          f"      v = exa_val_{pid}(T, q, A, exa_rank(T, A));"]
+    if full and layout.buckets[t]["base_k"]:
+        L.append(f"      exa_term_{pid}<EXA_M_JAC | EXA_M_HESS>(T, q, A, exa_rank(T, A), r);")
+    L += ["    } else {",
+          f"      const double xv = __ldg(A.x + (e & {(1 << 29) - 1} & ~(e >> 31)));",
+          f"      v = exa_bkval_T{t}(e, xv);"]
+    if full:
+        L.append(f"      if (e >= 0) exa_bkout_T{t}(e, xv, wrow, rc, A);")
+    L += ["    }",
+          "    const int d = __popc(__ballot_sync(0xffffffffu, e >= 0));  // entries in lanes 1..d",
+          "    double acc = lane == 0 ? 0.0 + v : v;",
+          "    for (int s = 1; s <= d; ++s) {",
+          "      const double up = __shfl_up_sync(0xffffffffu, acc, 1);",
+          "      if (lane == s) acc = up + v;",
+          "    }",
+          "    if (lane == d) A.c[T.row_offset + r] = acc;",
+          "    return;",
+          "  }"]
+    return L
+
+
+def _kernel_source(layout, m, half, kname) -> str:
+    """One entry kernel of a specialised module.
+
+    ``exa_vb_<kname>(b, tid, A)`` evaluates virtual CTA ``b`` (the segment
+    table's CTA numbering, ``threads`` threads).  Classic mode: one real CTA
+    per virtual CTA.  Persistent mode (``layout.persist[kid] = V > 0``): a
+    real CTA of ``V * threads`` threads holds V virtual CTAs; slot j of real
+    CTA c serves virtual CTAs ``c + G*j + G*V*k`` (G = gridDim.x, k = 0, 1,
+    ...), so every segment is spread over all SMs.  With ``EXA_TRACE`` each
+    warp records (SM, clock64 start, end, virtual CTA) per virtual CTA."""
+    kid = 2 * m + half
+    threads = layout.threads[half]
+    V = layout.persist[kid]
+    bounds = "@BOUNDS_H@" if half == 0 else "@BOUNDS_L@"
+    if V:
+        bounds = f"{threads * V}" + (f", {max(1, MIN_BLOCKS // V)}" if MIN_BLOCKS else "")
+    segs = layout.mode_segments(kid)
+    n_vb = sum((nrec + threads * rpt - 1) // (threads * rpt) for (_, _, _, nrec, rpt) in segs)
+    fn_body = [f"__device__ __forceinline__ void exa_vb_{kname}(const int b, const int tid, const ExaArgs& A) {{"]
+    for (t, kind, cta0, nrec, rpt) in segs:
+        n_cta = (nrec + threads * rpt - 1) // (threads * rpt)
+        b_ = [f"  if (b < {cta0 + n_cta}) {{"]
+        if kind & 15 == 4 and layout.buckets[t]["buckets"][kind >> 4]["d"] == 32:
+            fn_body += _warp_row_source(layout, t, kind >> 4, cta0, n_cta, threads, m == 0)
+            continue
+        if kind & 15 == 4:  # row bucket of augment-target block t: one thread per row
+            bk = layout.buckets[t]["buckets"][kind >> 4]
+            dd, n = bk["d"], bk["n"]
+            b_.append(f"    ExaTerm T; exa_init_T{t}(T, A);")
+            for i, off in enumerate(bk["f_off"]):
+                b_.append(f"    T.f[{i}] = A.f64 + {off}LL;")
+            for i, off in enumerate(bk["ix_off"]):
+                b_.append(f"    T.ix[{i}] = A.i32 + {off}LL;")
+            b_.append(f"    const int q = (b - {cta0}) * {threads} + tid;")
+            b_.append(f"    if (q >= {n}) return;")
+            b_.append(f"    const int r = __ldg(A.i32 + {bk['rows_off']}LL + q);")
+            # width class dd: entries k <= dd/2 always present, later ones may be -1
+            always = dd // 2 + 1 if dd > 1 else dd
+            full = m == 0  # set kernel: also the base term's and the augments' J/H slots
+            info = layout.buckets[t]
+            # chunks of 8 entries: loads, gathers (unconditional), in-order adds
+            for c0 in range(0, max(dd, 1), 8):
+                ks = range(c0, min(dd, c0 + 8))
+                for k in ks:
+                    b_.append(f"    const int e{k} = __ldg(A.i32 + {bk['ent_off'] + k * n}LL + q);")
+                    if full:
+                        b_.append(f"    const int rc{k} = __ldg(A.i32 + {bk['rec_off'] + k * n}LL + q);")
+                if c0 == 0:
+                    b_.append("    EXA_GRID_WAIT();")
+                    if full:
+                        b_.append("    const double wrow = __ldg(A.y + T.row_offset + r);")
+                        if info["base_k"]:
+                            b_.append(f"    exa_term_{layout.term_pid[t]}<EXA_M_JAC | EXA_M_HESS>(T, q, A, exa_rank(T, A), r);")
+                for k in ks:
+                    # pad entries (-1) gather x[0]: branch-free, selected away below
+                    b_.append(f"    const double xv{k} = __ldg(A.x + (e{k} & {(1 << 29) - 1} & ~(e{k} >> 31)));")
+                    b_.append(f"    const double v{k} = exa_bkval_T{t}(e{k}, xv{k});")
+                if c0 == 0:
+                    # reference order: zero-fill, base slice-add, augments in order (autodiff.py:573-580)
+                    b_.append(f"    double acc = 0.0 + exa_val_{layout.term_pid[t]}(T, q, A, exa_rank(T, A));")
+                for k in ks:
+                    if k < always:
+                        b_.append(f"    acc = acc + v{k};")
+                    else:
+                        b_.append(f"    acc = e{k} >= 0 ? acc + v{k} : acc;")
+                    if full:
+                        cond = "" if k < always else f"if (e{k} >= 0) "
+                        b_.append(f"    {cond}exa_bkout_T{t}(e{k}, xv{k}, wrow, rc{k}, A);")
+            b_.append("    A.c[T.row_offset + r] = acc;")
+            b_.append("    return;")
+            b_.append("  }")
+            fn_body += b_
+            continue
+        if kind == 3:  # term group: t is the group id
+            pid, grp, _ = layout.groups[t]
+            for gm, u in enumerate(grp):
+                b_.append(f"    ExaTerm T{gm}; exa_init_T{u}(T{gm}, A);")
+            tl = ", ".join(f"T{gm}" for gm in range(len(grp)))
+            rl = ", ".join(f"exa_rank(T{gm}, A)" for gm in range(len(grp)))
+            if rpt == 1:
+                b_.append(f"    const int r = (b - {cta0}) * {threads} + tid;")
+                b_.append(f"    if (r >= {nrec}) return;")
+                b_.append(f"    exa_grp_{t}<{_MODE_BITS[m]}>({tl}, r, A, {rl});")
+            else:
+                b_.append(f"    const int r0 = (b - {cta0}) * {threads * rpt} + tid;")
+                b_.append("#pragma unroll")
+                b_.append(f"    for (int q = 0; q < {rpt}; ++q) {{")
+                b_.append(f"      const int r = r0 + q * {threads};")
+                b_.append(f"      if (r < {nrec}) exa_grp_{t}<{_MODE_BITS[m]}>({tl}, r, A, {rl});")
+                b_.append("    }")
+        else:
+            b_.append(f"    ExaTerm T; exa_init_T{t}(T, A);")
+            if kind == 0:
+                b_.append(f"    const int r0 = (b - {cta0}) * {threads * rpt} + tid;")
+                b_.append("#pragma unroll")
+                b_.append(f"    for (int q = 0; q < {rpt}; ++q) {{")
+                b_.append(f"      const int r = r0 + q * {threads};")
+                b_.append(f"      if (r < {nrec}) exa_term_{layout.term_pid[t]}<{_MODE_BITS[m]}>(T, r, A, exa_rank(T, A));")
+                b_.append("    }")
+            else:  # fold rows are padded to whole warps: a warp never splits here
+                b_.append(f"    const int r = (b - {cta0}) * {threads} + tid;")
+                b_.append(f"    if (r >= {nrec}) return;")
+                fn = "exa_rowfold" if kind == 2 else "exa_row"
+                b_.append(f"    {fn}(T, r, A, [&](int u, int rec) {{ return exa_rowval_T{t}(u, rec, A); }});")
+        b_.append("    return;")
+        b_.append("  }")
+        fn_body += b_
+    fn_body.append("}")
+    body = [f"extern \"C\" __global__ void __launch_bounds__({bounds}) {kname}(",
+            "    const ExaTerm* __restrict__ terms, const ExaSeg* __restrict__ segs,",
+            "    const int* __restrict__ cta_seg, ExaArgs A) {"]
+    if V:
+        body += [f"  const int tid = (int)threadIdx.x % {threads};",
+                 f"  for (int b = (int)blockIdx.x + (int)gridDim.x * ((int)threadIdx.x / {threads}); b < {n_vb};"
+                 f" b += (int)gridDim.x * {V}) {{",
+                 "    EXA_TRACE_BEGIN();",
+                 f"    exa_vb_{kname}(b, tid, A);",
+                 f"    EXA_TRACE_END(b, tid, {threads});",
+                 "  }"]
+    else:
+        body += ["  EXA_TRACE_BEGIN();",
+                 f"  exa_vb_{kname}((int)blockIdx.x, (int)threadIdx.x, A);",
+                 f"  EXA_TRACE_END((int)blockIdx.x, (int)threadIdx.x, {threads});"]
+    # release the dependent grid only when this CTA's work is issued (an early
+    # release lets later grids' waiting CTAs take the slots this grid needs)
+    body.append("  EXA_GRID_RELEASE();")
+    body.append("}")
+    return "\n".join(fn_body) + "\n" + "\n".join(body)
 
 
 KERNEL_NAMES = ("exa_k_set", "exa_k_cons", "exa_k_jac", "exa_k_hess", "exa_k_objv", "exa_k_grad")
@@ -310,6 +522,8 @@ def module_source(patterns, meta_const: bool = True, layout=None) -> str:
     parts = ["// generated by paper_2510_12897_b200.jit",
              f"#define EXA_META_CONST {1 if (meta_const and layout is None) else 0}",
              f"#define EXA_PDL {1 if PDL else 0}",
+             f"#define EXA_TRACE {1 if TRACE else 0}",
+             f"#define EXA_TRACE_NT {max(THREADS, THREADS_HEAVY) * max(1, PERSIST)}",
              _inline_header("exa_device.h", seen), _inline_header("exa_math.h", seen), _PRELUDE]
     if SINCOS_IMPL == "cuda":
         parts.append("#define exa_sincos(x, s, c) sincos((x), (s), (c))")
