@@ -142,6 +142,15 @@ int exa_eval_hess(ExaPlan* plan, ExaWorkspace* ws, const double* x, const double
                   double obj_weight, double* hess, exa_stream_t stream);
 int exa_eval_set(ExaPlan* plan, ExaWorkspace* ws, const double* x, const double* mult,
                  double obj_weight, double* c, double* jac, double* hess, exa_stream_t stream);
+/* exa_eval_set with HOST buffers (the reference-facing drop-in path: numpy
+ * arrays in, numpy arrays out): copies x, mult to the workspace's device
+ * staging, evaluates, copies c, jac, hess back -- all asynchronous on
+ * `stream` (synchronise it before reading the outputs).  Pinned host memory
+ * makes the copies asynchronous, so sets on distinct workspaces and streams
+ * overlap their H2D copy, kernel and D2H copy. */
+int exa_eval_set_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, const double* mult_host,
+                      double obj_weight, double* c_host, double* jac_host, double* hess_host,
+                      exa_stream_t stream);
 /* out[k] = 0 + sum_{e in [ptr[k], ptr[k+1])} raw[ent[e]], sequentially in e
  * order (np.bincount order); with ent sorted by raw slot within each k this is
  * CompressedPattern.sum_values.  All pointers are device pointers. */

@@ -74,6 +74,8 @@ struct ExaWorkspace {
   unsigned long long* err = nullptr;
   cudaStream_t aux = nullptr;   // second stream: light kernel runs beside the heavy one
   cudaEvent_t fork = nullptr, join = nullptr;
+  /* device staging for exa_eval_set_host (allocated on first use) */
+  double *dx = nullptr, *dy = nullptr, *dc = nullptr, *dJ = nullptr, *dH = nullptr;
 };
 
 struct ExaPlan {
@@ -290,6 +292,11 @@ void exa_workspace_destroy(ExaWorkspace* w) {
   cudaFree(w->G);
   cudaFree(w->leafsum);
   cudaFree(w->err);
+  cudaFree(w->dx);
+  cudaFree(w->dy);
+  cudaFree(w->dc);
+  cudaFree(w->dJ);
+  cudaFree(w->dH);
   if (w->fork) cudaEventDestroy(w->fork);
   if (w->join) cudaEventDestroy(w->join);
   if (w->aux) cudaStreamDestroy(w->aux);
@@ -552,6 +559,28 @@ int exa_eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mu
   A.J = jac;
   A.H = hess;
   return launch_mode(p, w, EXA_MODE_SET, A, st);
+}
+
+int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
+                      double* jac, double* hess, exa_stream_t stream) {
+  if (!p) return fail("null plan");
+  ExaWorkspace* w = ws ? ws : p->dflt;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!w->dx) {  // first use: device staging sized for this plan
+    CU(cudaSetDevice(p->device));
+    CU(cudaMalloc((void**)&w->dx, (p->nvar > 0 ? p->nvar : 1) * sizeof(double)));
+    CU(cudaMalloc((void**)&w->dy, (p->ncon > 0 ? p->ncon : 1) * sizeof(double)));
+    CU(cudaMalloc((void**)&w->dc, (p->ncon > 0 ? p->ncon : 1) * sizeof(double)));
+    CU(cudaMalloc((void**)&w->dJ, (p->n_jac > 0 ? p->n_jac : 1) * sizeof(double)));
+    CU(cudaMalloc((void**)&w->dH, (p->n_hess > 0 ? p->n_hess : 1) * sizeof(double)));
+  }
+  if (p->nvar) CU(cudaMemcpyAsync(w->dx, x, p->nvar * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (p->ncon) CU(cudaMemcpyAsync(w->dy, mult, p->ncon * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (int rc = exa_eval_set(p, w, w->dx, w->dy, w_obj, w->dc, w->dJ, w->dH, stream)) return rc;
+  if (p->ncon) CU(cudaMemcpyAsync(c, w->dc, p->ncon * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (p->n_jac) CU(cudaMemcpyAsync(jac, w->dJ, p->n_jac * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (p->n_hess) CU(cudaMemcpyAsync(hess, w->dH, p->n_hess * sizeof(double), cudaMemcpyDeviceToHost, st));
+  return 0;
 }
 
 int exa_eval_cons(ExaPlan* p, ExaWorkspace* ws, const double* x, double* c, exa_stream_t stream) {

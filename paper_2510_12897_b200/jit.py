@@ -43,6 +43,7 @@ TRACE = os.environ.get("EXA_TRACE", "0") == "1"  # per-warp timeline (diagnostic
 # launch and first DRAM round trip (case13659: 8.8 -> 8.3 us per set).  The
 # library sets the launch attribute only for modules built with the waits.
 PDL = os.environ.get("EXA_PDL", "1") == "1"
+PDL_EARLY = os.environ.get("EXA_PDL_EARLY", "0") == "1"
 
 _lock = threading.Lock()
 _mem_cache: dict = {}
@@ -79,8 +80,16 @@ __device__ __forceinline__ void exa_report(const ExaArgs& A, int rank, int instr
 // programmatic dependent launch: release the next kernel early; wait for the
 // previous one before the first access to caller memory (x, y, outputs)
 #if EXA_PDL
+#if EXA_PDL_EARLY
+// release right after the wait: the next grid launches once every CTA of this
+// one is past its wait (so at most one grid runs ahead) and its resident CTAs
+// fetch their plan data while this grid computes
+#define EXA_GRID_WAIT() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+#define EXA_GRID_RELEASE() do {} while (0)
+#else
 #define EXA_GRID_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
 #define EXA_GRID_RELEASE() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+#endif
 #else
 #define EXA_GRID_WAIT() do {} while (0)
 #define EXA_GRID_RELEASE() do {} while (0)
@@ -522,6 +531,7 @@ def module_source(patterns, meta_const: bool = True, layout=None) -> str:
     parts = ["// generated by paper_2510_12897_b200.jit",
              f"#define EXA_META_CONST {1 if (meta_const and layout is None) else 0}",
              f"#define EXA_PDL {1 if PDL else 0}",
+             f"#define EXA_PDL_EARLY {1 if PDL_EARLY else 0}",
              f"#define EXA_TRACE {1 if TRACE else 0}",
              f"#define EXA_TRACE_NT {max(THREADS, THREADS_HEAVY) * max(1, PERSIST)}",
              _inline_header("exa_device.h", seen), _inline_header("exa_math.h", seen), _PRELUDE]

@@ -215,3 +215,38 @@ def test_domain_error_in_constraint_block_order():
     # sqrt (instr 1) fails before div (instr 4) in tape order; first bad record 1
     assert exc.value.op == "sqrt" and exc.value.record == 1 and exc.value.kind == "constraint"
     assert exc.value.block_index == 1
+
+
+@pytest.mark.parametrize("name", ["case14_polar", "case5_strg_mp4_polar"])
+def test_host_buffer_c_abi_matches_oracle(name):
+    """exa_eval_set_host (pinned host in/out, copies on the stream) returns the
+    CR oracle's bits, across two workspaces on two streams."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2510_12897_b200 import _lib
+
+    g = load(name)
+    model = build(name, lower_to_gpu=True, data=g)
+    x, y, w = g["x0"], g["y0"], float(g["w0"])
+    _, _, c0, J0, H0 = oracle_cr(model, x, y, w)
+    lib = _lib.load()
+    dp = model.device_plan
+    outs = []
+    for k in range(2):
+        wsp = C.c_void_p()
+        _lib.check(lib.exa_workspace_create(dp.handle, C.byref(wsp)), "workspace")
+        st = torch.cuda.Stream()
+        hx = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+        hy = torch.from_numpy(np.ascontiguousarray(y)).pin_memory()
+        hc = torch.empty(model.ncon, dtype=torch.float64).pin_memory()
+        hJ = torch.empty(model.plan.n_jac_slots, dtype=torch.float64).pin_memory()
+        hH = torch.empty(model.plan.n_hess_slots, dtype=torch.float64).pin_memory()
+        _lib.check(lib.exa_eval_set_host(dp.handle, wsp, hx.data_ptr(), hy.data_ptr(), w, hc.data_ptr(),
+                                         hJ.data_ptr(), hH.data_ptr(), C.c_void_p(st.cuda_stream)), "set_host")
+        st.synchronize()
+        lib.exa_workspace_destroy(wsp)
+        outs.append((hc.numpy().copy(), hJ.numpy().copy(), hH.numpy().copy()))
+    for c, J, H in outs:
+        assert bitwise_equal(c, c0) and bitwise_equal(J, J0) and bitwise_equal(H, H0)
