@@ -328,8 +328,9 @@ class HostLayout:
                         lst.append({
                             "d": dd, "n": int(rows.size),
                             "rows_off": i32.add(_i32(rows, "bucket rows")),
-                            "ent_off": i32.add(_i32(ent.reshape(-1), "bucket entries")) if dd else -1,
-                            "rec_off": i32.add(_i32(rec.reshape(-1), "bucket records")) if dd else -1,
+                            # (entry, record) int2 pairs: one 8-byte load per contribution
+                            "pair_off": i32.add(_i32(np.stack([ent, rec], axis=-1).reshape(-1), "bucket entries"))
+                            if dd else -1,
                             "f_off": [f64.add(np.asarray(tp.reals[nm])[rows]) for nm in tp.tape.field_names],
                             "ix_off": [i32.add(_i32(np.asarray(tp.table.indices[nm])[rows], f"index column {nm!r}"))
                                        for nm in tp.tape.index_names],

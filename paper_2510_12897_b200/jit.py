@@ -357,9 +357,10 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, full):
           "    const int lane = tid & 31;",
           f"    if (q >= {n}) return;  // warp-uniform",
           f"    const int r = __ldg(A.i32 + {bk['rows_off']}LL + q);",
-          f"    const int e = __ldg(A.i32 + {bk['ent_off']}LL + 32 * q + lane);"]
+          f"    const int2 er = __ldg(reinterpret_cast<const int2*>(A.i32 + {bk['pair_off']}LL) + 32 * q + lane);",
+          "    const int e = er.x;"]
     if full:
-        L.append(f"    const int rc = __ldg(A.i32 + {bk['rec_off']}LL + 32 * q + lane);")
+        L.append("    const int rc = er.y;")
     L.append("    EXA_GRID_WAIT();")
     if full:
         L.append("    const double wrow = __ldg(A.y + T.row_offset + r);")
@@ -430,20 +431,24 @@ def _kernel_source(layout, m, half, kname) -> str:
             for c0 in range(0, max(dd, 1), 8):
                 ks = range(c0, min(dd, c0 + 8))
                 for k in ks:
-                    b_.append(f"    const int e{k} = __ldg(A.i32 + {bk['ent_off'] + k * n}LL + q);")
-                    if full:
-                        b_.append(f"    const int rc{k} = __ldg(A.i32 + {bk['rec_off'] + k * n}LL + q);")
+                    b_.append(f"    const int2 er{k} = __ldg(reinterpret_cast<const int2*>(A.i32 + {bk['pair_off']}LL) + {k * n} + q);")
+                    b_.append(f"    const int e{k} = er{k}.x, rc{k} = er{k}.y;")
                 if c0 == 0:
+                    b_.append(f"    EXA_TP(0, {'e0' if dd else 'r'});")
                     b_.append("    EXA_GRID_WAIT();")
                     if full:
                         b_.append("    const double wrow = __ldg(A.y + T.row_offset + r);")
-                        if info["base_k"]:
-                            b_.append(f"    exa_term_{layout.term_pid[t]}<EXA_M_JAC | EXA_M_HESS>(T, q, A, exa_rank(T, A), r);")
                 for k in ks:
                     # pad entries (-1) gather x[0]: branch-free, selected away below
                     b_.append(f"    const double xv{k} = __ldg(A.x + (e{k} & {(1 << 29) - 1} & ~(e{k} >> 31)));")
                     b_.append(f"    const double v{k} = exa_bkval_T{t}(e{k}, xv{k});")
                 if c0 == 0:
+                    if ks:
+                        b_.append("    EXA_TP(1, " + " + ".join(f"xv{k}" for k in ks) + ");")
+                    # base term J/H after the entry gathers are issued (in-order issue:
+                    # its stores wait on its own gather and would hold the others back)
+                    if full and info["base_k"]:
+                        b_.append(f"    exa_term_{layout.term_pid[t]}<EXA_M_JAC | EXA_M_HESS>(T, q, A, exa_rank(T, A), r);")
                     # reference order: zero-fill, base slice-add, augments in order (autodiff.py:573-580)
                     b_.append(f"    double acc = 0.0 + exa_val_{layout.term_pid[t]}(T, q, A, exa_rank(T, A));")
                 for k in ks:

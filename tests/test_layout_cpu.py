@@ -28,9 +28,10 @@ def _bucket_cons(model, x):
         for bk in info["buckets"]:
             W, n = bk["d"], bk["n"]
             rows = lay.i32[bk["rows_off"]:bk["rows_off"] + n]
-            ent = lay.i32[bk["ent_off"]:bk["ent_off"] + W * n].reshape(W, n) if W else np.zeros((0, n), np.int32)
+            pairs = lay.i32[bk["pair_off"]:bk["pair_off"] + 2 * W * n] if W else np.zeros(0, np.int32)
+            ent = pairs[0::2].reshape(W, n) if W else np.zeros((0, n), np.int32)
             if W == 32:  # long rows: (n, 32) row-major, lane 0 = base
-                ent = lay.i32[bk["ent_off"]:bk["ent_off"] + W * n].reshape(n, 32).T
+                ent = pairs[0::2].reshape(n, 32).T
             for q in range(n):
                 r = int(rows[q])
                 acc = 0.0 + float(vals[t][r])
@@ -64,8 +65,8 @@ def test_bucket_layout_reproduces_reference_row_order():
             W, n = bk["d"], bk["n"]
             if not W:
                 continue
-            ent = lay.i32[bk["ent_off"]:bk["ent_off"] + W * n]
-            rec = lay.i32[bk["rec_off"]:bk["rec_off"] + W * n]
+            pairs = lay.i32[bk["pair_off"]:bk["pair_off"] + 2 * W * n]
+            ent, rec = pairs[0::2], pairs[1::2]
             assert np.array_equal(ent < 0, rec < 0)
             for sel, u in enumerate(info["augs"]):
                 seen[u].append(rec[(ent >= 0) & ((ent >> BUCKET_GID_BITS) == sel)])

@@ -37,7 +37,7 @@ for s in range(len(segs)):
         continue
     rel = [(ph[m, k] - c0[m]) / 1965.0 for k in range(3)]
     print(f"seg {s:3d} phases (us from warp start): loads {rel[0].mean():.2f}  gathers {rel[1].mean():.2f}"
-          f"  sincos {rel[2].mean():.2f}  end {dur[m].mean():.2f}")
+          f"  p2 {rel[2][ph[m, 2] > 0].mean() if (ph[m, 2] > 0).any() else float('nan'):.2f}  end {dur[m].mean():.2f}")
 T = np.linspace(0, ge[ok].max(), 40)
 conc = [((gs[ok] <= x) & (ge[ok] > x)).sum() for x in T]
 print("warps in flight over time:", " ".join(str(c) for c in conc))
