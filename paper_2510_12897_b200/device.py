@@ -29,7 +29,7 @@ import numpy as np
 from . import _lib
 from .codegen import PatternCode
 from .core import ModelError
-from .jit import PDL, PERSIST, THREADS, THREADS_HEAVY, compile_module, module_source
+from .jit import PDL, PERSIST, THREADS_ENV, THREADS_HEAVY, choose_threads, compile_module, module_source
 
 ALIGN = 32  # elements: 256 B for fp64, 128 B for int32
 
@@ -271,7 +271,7 @@ class HostLayout:
 
     def __init__(self, plan):
         self.plan = plan
-        self.threads = (THREADS_HEAVY, THREADS)
+        self.env_sig = (THREADS_ENV, THREADS_HEAVY, PDL)
         terms = plan.obj_terms + plan.con_terms
         self.terms = terms
         n_obj = len(plan.obj_terms)
@@ -431,6 +431,7 @@ class HostLayout:
         # slots, small CTAs so the few heavy CTAs spread evenly over the 148
         # SMs) and a light kernel (everything else, big CTAs, few registers);
         # kernel id = 2 * mode + {0 heavy, 1 light}.  They run concurrently.
+        self.threads = (THREADS_HEAVY, choose_threads(sum(sg[2] for sg in segs[_lib.MODE_SET])))
         self.segs = {}
         self.n_ctas = []
         for m in range(_lib.NMODES):
@@ -477,7 +478,7 @@ class HostLayout:
         self.persist = [PERSIST if (self.specialised and self.n_ctas[kid]) else 0 for kid in range(_lib.NKERN)]
         self.pdl = PDL
         self.source = module_source(self.patterns, meta_const=False,
-                                    layout=self if self.specialised else None)
+                                    layout=self if self.specialised else None, threads=self.threads[1])
 
     def _make_groups(self, terms, descs):
         import hashlib
@@ -596,7 +597,7 @@ class HostLayout:
 
 def host_layout(plan) -> HostLayout:
     lay = getattr(plan, "_exa_layout", None)
-    if lay is None or lay.threads != (THREADS_HEAVY, THREADS) or lay.pdl != PDL:
+    if lay is None or lay.env_sig != (THREADS_ENV, THREADS_HEAVY, PDL):
         lay = HostLayout(plan)
         plan._exa_layout = lay
     return lay

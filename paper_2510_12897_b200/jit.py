@@ -26,10 +26,26 @@ CSRC = Path(__file__).resolve().parent / "csrc"
 CACHE_DIR = Path(os.environ.get("EXA_JIT_CACHE", Path(__file__).resolve().parent / "_jit"))
 NVRTC_OPTIONS = ("-arch=sm_100a", "--fmad=false", "-default-device", "-std=c++17", "-lineinfo",
                  "--extra-device-vectorization")
-THREADS = int(os.environ.get("EXA_THREADS", "32"))  # CTA size (fused / light kernels)
-THREADS_HEAVY = int(os.environ.get("EXA_THREADS_HEAVY", "128"))  # heavy kernels
+# CTA size of the fused kernels: "auto" = 32 threads when the whole set fits
+# one wave of 32-thread CTAs (single instances: fine-grained balance of the
+# long flow CTAs over the SMs), else 256 (batched sets of many waves: fewer
+# CTA launches; N-1 1024 x case2000 1187 -> 1011 us, MP96 46.0 -> 43.8 us)
+THREADS_ENV = os.environ.get("EXA_THREADS", "auto")
+THREADS_HEAVY = int(os.environ.get("EXA_THREADS_HEAVY", "128"))  # heavy kernels (EXA_SPLIT experiment)
+SM_COUNT = 148
 # tuning knobs (experiments only; defaults are the product configuration)
-MIN_BLOCKS = int(os.environ.get("EXA_MINB", str(1024 // THREADS)))  # 1024 threads/SM -> <= 64 regs
+MINB_ENV = os.environ.get("EXA_MINB")  # default: 1024 threads/SM -> <= 64 registers
+
+
+def choose_threads(n_threads: int) -> int:
+    """CTA size for a set kernel that needs ``n_threads`` threads in total."""
+    if THREADS_ENV != "auto":
+        return int(THREADS_ENV)
+    return 32 if (n_threads + 31) // 32 <= SM_COUNT * 32 else 256
+
+
+def min_blocks(threads: int) -> int:
+    return int(MINB_ENV) if MINB_ENV is not None else max(1, 1024 // threads)
 SINCOS_IMPL = os.environ.get("EXA_SINCOS_IMPL", "cr")  # "cuda" = libdevice sincos, NOT parity-exact
 # Persistent specialised kernels (experiment, off): each real CTA runs PERSIST
 # virtual CTAs of THREADS threads side by side and strides over the model's
@@ -402,7 +418,7 @@ def _kernel_source(layout, m, half, kname) -> str:
     V = layout.persist[kid]
     bounds = "@BOUNDS_H@" if half == 0 else "@BOUNDS_L@"
     if V:
-        bounds = f"{threads * V}" + (f", {max(1, MIN_BLOCKS // V)}" if MIN_BLOCKS else "")
+        bounds = f"{threads * V}, {max(1, min_blocks(threads) // V)}"
     segs = layout.mode_segments(kid)
     n_vb = sum((nrec + threads * rpt - 1) // (threads * rpt) for (_, _, _, nrec, rpt) in segs)
     fn_body = [f"__device__ __forceinline__ void exa_vb_{kname}(const int b, const int tid, const ExaArgs& A) {{"]
@@ -524,7 +540,7 @@ def _kernel_source(layout, m, half, kname) -> str:
 KERNEL_NAMES = ("exa_k_set", "exa_k_cons", "exa_k_jac", "exa_k_hess", "exa_k_objv", "exa_k_grad")
 
 
-def module_source(patterns, meta_const: bool = True, layout=None) -> str:
+def module_source(patterns, meta_const: bool = True, layout=None, threads: int = 32) -> str:
     """CUDA source of a model's module.
 
     ``layout`` given -> *model-specialised* module: term metadata and the
@@ -538,7 +554,7 @@ def module_source(patterns, meta_const: bool = True, layout=None) -> str:
              f"#define EXA_PDL {1 if PDL else 0}",
              f"#define EXA_PDL_EARLY {1 if PDL_EARLY else 0}",
              f"#define EXA_TRACE {1 if TRACE else 0}",
-             f"#define EXA_TRACE_NT {max(THREADS, THREADS_HEAVY) * max(1, PERSIST)}",
+             f"#define EXA_TRACE_NT {max(threads, THREADS_HEAVY) * max(1, PERSIST)}",
              _inline_header("exa_device.h", seen), _inline_header("exa_math.h", seen), _PRELUDE]
     if SINCOS_IMPL == "cuda":
         parts.append("#define exa_sincos(x, s, c) sincos((x), (s), (c))")
@@ -554,7 +570,7 @@ def module_source(patterns, meta_const: bool = True, layout=None) -> str:
         parts.append(_ENTRIES)
     else:
         parts.append(_specialised_kernels(layout))
-    bl = f"{THREADS}, {MIN_BLOCKS}" if MIN_BLOCKS else str(THREADS)
+    bl = f"{threads}, {min_blocks(threads)}"
     return "\n".join(parts).replace("@BOUNDS_L@", bl).replace("@BOUNDS_H@", str(THREADS_HEAVY))
 
 

@@ -76,6 +76,6 @@ with torch.cuda.stream(st):
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / (5 * S * R)
 info = plans[0].info()
-print(json.dumps({"workload": name, "mode": mode, "bytes": bps, "R": R, "threads": jit.THREADS, "minb": jit.MIN_BLOCKS,
+print(json.dumps({"workload": name, "mode": mode, "bytes": bps, "R": R, "threads": plans[0].layout.threads[1], "minb": jit.MINB_ENV,
                   "sincos": jit.SINCOS_IMPL, "persist": jit.PERSIST, "pdl": jit.PDL, "env": {k: v for k, v in os.environ.items() if k.startswith("EXA_")}, "us_per_set": us, "GBps": bps / us / 1e3,
                   "regs": info["regs_set_kernel"], "ctas": info["ctas"], "jit_s": tjit}), flush=True)
