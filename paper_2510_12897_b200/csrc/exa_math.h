@@ -24,7 +24,11 @@
 
 #if defined(__CUDACC_RTC__) || defined(__CUDACC__)
 #define EXA_FN __device__ __forceinline__
+#if defined(EXA_SC_CONST)
+#define EXA_TABLE_QUAL __constant__ const
+#else
 #define EXA_TABLE_QUAL __device__ const
+#endif
 #else
 #include <math.h>
 #define EXA_FN static inline
@@ -122,39 +126,18 @@ EXA_FN void exa_sincos_reduced(exa_dd r, exa_dd* s_out, exa_dd* c_out) {
   *c_out = cr;
 }
 
-/* Half an ulp of |v| (v normal, finite). */
-EXA_FN double exa_half_ulp(double v) {
-#if defined(__CUDACC_RTC__) || defined(__CUDACC__)
-  long long b = __double_as_longlong(v) & 0x7ff0000000000000LL;
-  return __longlong_as_double(b) * 0x1p-53;
-#else
-  union { double d; long long i; } u;
-  u.d = v;
-  u.i &= 0x7ff0000000000000LL;
-  return u.d * 0x1p-53;
-#endif
-}
-
-EXA_FN int exa_mant_zero(double v) {
-#if defined(__CUDACC_RTC__) || defined(__CUDACC__)
-  return (__double_as_longlong(v) & 0x000fffffffffffffLL) == 0;
-#else
-  union { double d; long long i; } u;
-  u.d = v;
-  return (u.i & 0x000fffffffffffffLL) == 0;
-#endif
-}
-
 /* Round h + t (|t| << |h|) to nearest when the exact value is known to lie
- * within err of h + t; returns 0 when the rounding cannot be decided. */
+ * within err of h + t; returns 0 when the rounding cannot be decided.
+ * Ziv's endpoint test: rounding is monotone, so if both ends of an interval
+ * containing the exact value round to the same double, that double is the
+ * correctly rounded result.  The ends h + (t +- E) are computed in double;
+ * E = err + 2^-51 (|t| + err) absorbs the rounding of t +- E itself. */
 EXA_FN int exa_round_decided(double h, double t, double err, double* out) {
-  exa_dd n = exa_fast_two_sum(h, t);
-  if (exa_mant_zero(n.hi)) return 0; /* binade edge: let the slow path decide */
-  if (fabs(n.lo) + err < exa_half_ulp(n.hi)) {
-    *out = n.hi;
-    return 1;
-  }
-  return 0;
+  const double E = fma(0x1p-51, fabs(t) + err, err);
+  const double hi = h + (t + E);
+  const double lo = h + (t - E);
+  *out = hi;
+  return hi == lo;
 }
 
 /* Fast path for |x| <= pi/4 (Ziv's strategy): the result is returned only
@@ -224,26 +207,20 @@ EXA_FN int exa_sincos_fast(double ax, double* s_out, double* c_out) {
   return 1;
 }
 
-/* Correctly rounded (barring hard cases) sin and cos of x. */
-EXA_FN void exa_sincos(double x, double* s_out, double* c_out) {
+/* Everything but the fast path, out of line: the rarely taken reduction,
+ * double-double evaluation and platform fallback must not shape the register
+ * allocation (spills, call frames) of the inlined fast path. */
+#if defined(__CUDACC_RTC__) || defined(__CUDACC__)
+__device__ __noinline__
+#else
+static
+#endif
+void exa_sincos_slow(double x, double* s_out, double* c_out) {
   double ax = fabs(x);
   if (!(ax <= 0x1.921fb54442d18p+20)) { /* NaN, inf, or huge: platform fallback */
     *s_out = sin(x);
     *c_out = cos(x);
     return;
-  }
-  if (ax < 0x1p-27) {
-    *s_out = x;
-    *c_out = 1.0;
-    return;
-  }
-  if (ax <= EXA_PIO4) {
-    double sf, cf;
-    if (exa_sincos_fast(ax, &sf, &cf)) {
-      *s_out = x < 0.0 ? -sf : sf;
-      *c_out = cf;
-      return;
-    }
   }
   exa_dd r;
   int q = 0;
@@ -269,6 +246,18 @@ EXA_FN void exa_sincos(double x, double* s_out, double* c_out) {
   }
   *s_out = x < 0.0 ? -sr : sr;
   *c_out = cr;
+}
+
+/* Correctly rounded (barring hard cases) sin and cos of x. */
+EXA_FN void exa_sincos(double x, double* s_out, double* c_out) {
+  const double ax = fabs(x);
+  double sf, cf;
+  if (ax <= EXA_PIO4 && exa_sincos_fast(ax, &sf, &cf)) {
+    *s_out = x < 0.0 ? -sf : sf;
+    *c_out = cf;
+    return;
+  }
+  exa_sincos_slow(x, s_out, c_out);
 }
 
 EXA_FN double exa_sin(double x) {

@@ -46,6 +46,7 @@ def choose_threads(n_threads: int) -> int:
 
 def min_blocks(threads: int) -> int:
     return int(MINB_ENV) if MINB_ENV is not None else max(1, 1024 // threads)
+SC_TABLE = os.environ.get("EXA_SC_TABLE", "global")  # sin/cos table: "global" (L1/L2) or "const"
 SINCOS_IMPL = os.environ.get("EXA_SINCOS_IMPL", "cr")  # "cuda" = libdevice sincos, NOT parity-exact
 # Persistent specialised kernels (experiment, off): each real CTA runs PERSIST
 # virtual CTAs of THREADS threads side by side and strides over the model's
@@ -554,6 +555,7 @@ def module_source(patterns, meta_const: bool = True, layout=None, threads: int =
              f"#define EXA_PDL {1 if PDL else 0}",
              f"#define EXA_PDL_EARLY {1 if PDL_EARLY else 0}",
              f"#define EXA_TRACE {1 if TRACE else 0}",
+             "#define EXA_SC_CONST 1" if SC_TABLE == "const" else "",
              f"#define EXA_TRACE_NT {max(threads, THREADS_HEAVY) * max(1, PERSIST)}",
              _inline_header("exa_device.h", seen), _inline_header("exa_math.h", seen), _PRELUDE]
     if SINCOS_IMPL == "cuda":
