@@ -157,6 +157,16 @@ int exa_eval_set_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, con
 int exa_segment_sum(int64_t nnz, const int64_t* ptr, const int32_t* ent, const double* raw,
                     double* out, exa_stream_t stream);
 
+/* Solver-side consumer of the compressed callbacks: the
+ * values of the reference IPM's KKT matrix (solver.py:421-456: H block
+ * W + W^T - diag W, + sigma on the primal/slack diagonal, Jacobian and slack
+ * coupling blocks, fixed rows/columns, + delta_w on free diagonals, - delta_c
+ * on the dual diagonal) in a lower-triangle CSR whose pattern and per-entry
+ * descriptors (int32 pairs, see kkt.py) are built once on the host.  All
+ * pointers are device pointers; bit-identical to the reference's dense K. */
+int exa_kkt_values(int64_t n, const int32_t* desc, const double* hvals, const double* jvals,
+                   const double* sigma, double delta_w, double delta_c, double* out, exa_stream_t stream);
+
 /* Synchronises `stream`; returns 1 and fills the location if the last
  * evaluation on `ws` hit a numeric-domain violation, 0 if not, < 0 on error.
  * rank = term rank in the callback's evaluation order, instr = tape index,

@@ -72,6 +72,7 @@ SIGNATURES = {
     "exa_eval_set": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp, vp, vp]),
     "exa_eval_set_host": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp, vp, vp]),
     "exa_segment_sum": (C.c_int, [i64, vp, vp, vp, vp, vp]),
+    "exa_kkt_values": (C.c_int, [i64, vp, vp, vp, vp, dbl, dbl, vp, vp]),
     "exa_domain_error": (C.c_int, [vp, vp, vp, C.POINTER(i64), C.POINTER(i32), C.POINTER(i64)]),
     "exa_last_error": (C.c_char_p, []),
     "exa_device_sincos": (C.c_int, [vp, vp, vp, i64, vp]),

@@ -205,6 +205,38 @@ __global__ void exa_compress_reduce(int64_t nnz, const int64_t* __restrict__ ptr
   out[k] = acc;
 }
 
+// KKT assembly (reference solver.py:421-456): one thread per lower-triangle
+// CSR entry; desc = (kind << 29 | a, b).  Kinds and their exact arithmetic:
+//   0 H off-diagonal        (h + 0) - 0              (W + W^T - diag W)
+//   1 diagonal with H       (((h + h) - h) + sigma[b]) + delta_w
+//   2 diagonal without H    (0 + sigma[b]) + delta_w
+//   3 Jacobian              j
+//   4 slack coupling        -1
+//   5 dual diagonal         delta_c != 0 ? 0 - delta_c : 0
+//   6 fixed row/col         0
+//   7 fixed diagonal        1
+__global__ void exa_kkt_kernel(int64_t n, const int2* __restrict__ desc, const double* __restrict__ h,
+                               const double* __restrict__ j, const double* __restrict__ sigma, double dw,
+                               double dc, double* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int2 d = __ldg(desc + p);
+  const int kind = (int)((unsigned)d.x >> 29);
+  const int a = d.x & ((1 << 29) - 1);
+  double v;
+  switch (kind) {
+    case 0: { const double hv = __ldg(h + a); v = (hv + 0.0) - 0.0; break; }
+    case 1: { const double hv = __ldg(h + a); v = (((hv + hv) - hv) + __ldg(sigma + d.y)) + dw; break; }
+    case 2: v = (0.0 + __ldg(sigma + d.y)) + dw; break;
+    case 3: v = __ldg(j + a); break;
+    case 4: v = -1.0; break;
+    case 5: v = dc != 0.0 ? 0.0 - dc : 0.0; break;
+    case 6: v = 0.0; break;
+    default: v = 1.0; break;
+  }
+  out[p] = v;
+}
+
 __global__ void exa_sincos_kernel(const double* __restrict__ x, double* __restrict__ s, double* __restrict__ c,
                                   int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -636,6 +668,17 @@ int exa_eval_grad(ExaPlan* p, ExaWorkspace* ws, const double* x, double* g, exa_
       CU(cudaMemsetAsync(g, 0, p->nvar * sizeof(double), st));
     }
   }
+  return 0;
+}
+
+int exa_kkt_values(int64_t n, const int32_t* desc, const double* hvals, const double* jvals, const double* sigma,
+                   double delta_w, double delta_c, double* out, exa_stream_t stream) {
+  if (n < 0) return fail("exa_kkt_values: negative size");
+  if (n == 0) return 0;
+  if (!desc || !out || !sigma) return fail("exa_kkt_values: null argument");
+  exa_kkt_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, reinterpret_cast<const int2*>(desc), hvals, jvals,
+                                                                    sigma, delta_w, delta_c, out);
+  CU(cudaGetLastError());
   return 0;
 }
 
