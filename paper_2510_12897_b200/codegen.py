@@ -635,6 +635,9 @@ class PatternCode:
             gradx = self._slot_sums(gx, adjx)
             tx = self._tangents(gx, vx, 0)
             colx = self._slot_sums(gx, self._adjoint_tangents(gx, vx, adjx, tx))
+            # x-independent J/H (pg, -p, ...: +-1 and w * 0): row buckets store
+            # them before gathering the variable
+            self.termx_const = not isinstance(gradx[0], Sym) and not isinstance(colx[0], Sym)
             out.append(f"__device__ __forceinline__ void exa_termx_{pid}(const double x0, const double wgt, double& jv, double& hv) {{")
             out.extend(gx.lines)
             out.append(f"  jv = {R(gradx[0])};")
@@ -708,6 +711,14 @@ def group_source(gid: int, entries: list) -> str:
     # Stores are emitted as soon as their value is final (cons after the
     # value pass, J after the adjoint sweep, each Hessian column after its
     # seed's sweep) so that the LSU drains while the next sweep computes.
+    # Stores whose value does not depend on x (constant J entries, structural
+    # Hessian zeros w * 0) go right after the weight loads: their DRAM write
+    # traffic then overlaps the gather phase instead of queueing behind it.
+    early: list = []
+
+    def const(v) -> bool:
+        return not isinstance(v, Sym)
+
     for m, (pc, mem) in enumerate(entries):
         k = pc.k
         T = f"T{m}"
@@ -723,18 +734,21 @@ def group_source(gid: int, entries: list) -> str:
         adj = pc._adjoints(g, v)
         grads = pc._slot_sums(g, adj)
         for s_ in range(k):
-            g.lines.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
-            g.lines.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
+            dst = early if const(grads[s_]) else g.lines
+            dst.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
+            dst.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
         for seed in range(k):
             t = pc._tangents(g, v, seed)
             col = pc._slot_sums(g, pc._adjoint_tangents(g, v, adj, t))
             j = seed
             for i in range(j, k):
                 expr = R(col[i])
-                if i != j and pc.slot_struct[i][0] == pc.slot_struct[j][0]:
+                dup = i != j and pc.slot_struct[i][0] == pc.slot_struct[j][0]
+                if dup:
                     expr = f"({cnames[m][i]} == {cnames[m][j]} ? {expr} * 2.0 : {expr})"
                 pair = i * (i + 1) // 2 + j
-                g.lines.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
+                dst = early if (const(col[i]) and not dup) else g.lines
+                dst.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
     args = ", ".join(f"const ExaTerm& T{m}" for m in range(M))
     ranks = ", ".join(f"int rank{m}" for m in range(M))
     out = [f"template <int MODE>\n__device__ __forceinline__ void exa_grp_{gid}({args}, int r, const ExaArgs& A, {ranks}) {{",
@@ -744,6 +758,7 @@ def group_source(gid: int, entries: list) -> str:
     out.append(f"  EXA_TP(0, i{min(u_src)});" if u_src else "  EXA_TP(0, 0.0);")
     out.append("  EXA_GRID_WAIT();")
     out.extend(post)
+    out.extend(early)
     if xkey:
         out.append("  EXA_TP(1, " + " + ".join(f"xg{n}" for n in range(len(xkey))) + ");")
     # phase stamp 2 after the first sin/cos

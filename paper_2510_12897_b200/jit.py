@@ -54,6 +54,7 @@ SINCOS_IMPL = os.environ.get("EXA_SINCOS_IMPL", "cr")  # "cuda" = libdevice sinc
 # assignment cannot balance the long flow CTAs).
 PERSIST = int(os.environ.get("EXA_PERSIST", "0"))
 TRACE = os.environ.get("EXA_TRACE", "0") == "1"  # per-warp timeline (diagnostics builds)
+BUCKET_EARLY_OUT = os.environ.get("EXA_BUCKET_EARLY_OUT", "0") == "1"  # experiment
 # Programmatic dependent launch: a CTA releases the next grid once its work is
 # issued; the next grid's CTAs load their (immutable) plan data before
 # griddepcontrol.wait, so back-to-back sets overlap one's drain with the next's
@@ -390,7 +391,7 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, full):
           f"      const double xv = __ldg(A.x + (e & {(1 << 29) - 1} & ~(e >> 31)));",
           f"      v = exa_bkval_T{t}(e, xv);"]
     if full:
-        L.append(f"      if (e >= 0) exa_bkout_T{t}(e, xv, wrow, rc, A);")
+        L.append(f"      if (e >= 0) exa_bkout_T{t}(e, xv, wrow, rc, A);")  # (constant J/H: hoisted by the compiler)
     L += ["    }",
           "    const int d = __popc(__ballot_sync(0xffffffffu, e >= 0));  // entries in lanes 1..d",
           "    double acc = lane == 0 ? 0.0 + v : v;",
@@ -444,6 +445,10 @@ def _kernel_source(layout, m, half, kname) -> str:
             always = dd // 2 + 1 if dd > 1 else dd
             full = m == 0  # set kernel: also the base term's and the augments' J/H slots
             info = layout.buckets[t]
+            # (storing x-independent augment J/H before the gathers was measured
+            # slower: the scattered stores delay the row's gathers)
+            early_out = BUCKET_EARLY_OUT and all(getattr(layout.patterns[layout.term_pid[u]], "termx_const", False)
+                                                 for u in info["augs"])
             # chunks of 8 entries: loads, gathers (unconditional), in-order adds
             for c0 in range(0, max(dd, 1), 8):
                 ks = range(c0, min(dd, c0 + 8))
@@ -458,6 +463,12 @@ def _kernel_source(layout, m, half, kname) -> str:
                 for k in ks:
                     # pad entries (-1) gather x[0]: branch-free, selected away below
                     b_.append(f"    const double xv{k} = __ldg(A.x + (e{k} & {(1 << 29) - 1} & ~(e{k} >> 31)));")
+                if full and early_out:
+                    # x-independent augment J/H: stored while the gathers are in flight
+                    for k in ks:
+                        cond = "" if k < always else f"if (e{k} >= 0) "
+                        b_.append(f"    {cond}exa_bkout_T{t}(e{k}, 0.0, wrow, rc{k}, A);")
+                for k in ks:
                     b_.append(f"    const double v{k} = exa_bkval_T{t}(e{k}, xv{k});")
                 if c0 == 0:
                     if ks:
@@ -473,7 +484,7 @@ def _kernel_source(layout, m, half, kname) -> str:
                         b_.append(f"    acc = acc + v{k};")
                     else:
                         b_.append(f"    acc = e{k} >= 0 ? acc + v{k} : acc;")
-                    if full:
+                    if full and not early_out:
                         cond = "" if k < always else f"if (e{k} >= 0) "
                         b_.append(f"    {cond}exa_bkout_T{t}(e{k}, xv{k}, wrow, rc{k}, A);")
             b_.append("    A.c[T.row_offset + r] = acc;")
