@@ -660,7 +660,7 @@ class PatternCode:
         return list(self.tape.instr)
 
 
-def group_source(gid: int, entries: list) -> str:
+def group_source(gid: int, entries: list, augs: list = ()) -> str:
     """One thread evaluates record r of several terms (a *term group*).
 
     ``entries[m] = (PatternCode, {"cols": [group column id per index column],
@@ -670,7 +670,13 @@ def group_source(gid: int, entries: list) -> str:
     content are loaded once, variables with the same (block, column) are
     gathered once, and every identical sub-expression -- e.g. sin/cos(va_f -
     va_t) -- is computed once (the generator's CSE), while each member's
-    outputs keep the reference's per-term operation order."""
+    outputs keep the reference's per-term operation order.
+
+    ``augs[k] = (PatternCode, record offset, member, slot)``: in the set kernel
+    the group also writes the J/H slots of augment ``U<k>``'s records
+    ``off + r`` (single-variable, field-free pattern gathering the same
+    variable as the member's slot), weighted by the multiplier of the row the
+    augment record adds into."""
     M = len(entries)
     g = Gen()
     pre, post = [], []
@@ -749,7 +755,17 @@ def group_source(gid: int, entries: list) -> str:
                 pair = i * (i + 1) // 2 + j
                 dst = early if (const(col[i]) and not dup) else g.lines
                 dst.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
-    args = ", ".join(f"const ExaTerm& T{m}" for m in range(M))
+    # attached augments (set kernel only): J/H of records off + r
+    SET = "(MODE == (EXA_M_CONS | EXA_M_JAC | EXA_M_HESS))"
+    aug_late = []
+    for k, (apc, off, m, s_) in enumerate(augs):
+        xs = vsyms[m][s_].name
+        post.append(f"  const double wa{k} = !{SET} ? 0.0 : __ldg(A.y + __ldg(U{k}.rows + {off} + r));")
+        dst = early if getattr(apc, "termx_const", False) else aug_late
+        dst.append(f"  if {SET} {{ double jv, hv; exa_termx_{apc.pid}({xs}, wa{k}, jv, hv); "
+                   f"Jout[U{k}.jac0 + {off}LL + r] = jv; Hout[U{k}.hess0 + {off}LL + r] = hv; }}")
+    g.lines.extend(aug_late)
+    args = ", ".join([f"const ExaTerm& T{m}" for m in range(M)] + [f"const ExaTerm& U{k}" for k in range(len(augs))])
     ranks = ", ".join(f"int rank{m}" for m in range(M))
     out = [f"template <int MODE>\n__device__ __forceinline__ void exa_grp_{gid}({args}, int r, const ExaArgs& A, {ranks}) {{",
            "  double* __restrict__ Cout = A.c;", "  double* __restrict__ Jout = A.J;",

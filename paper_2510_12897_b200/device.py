@@ -51,6 +51,7 @@ BUCKET_MAX_N = 48                      # at most this many distinct counts per b
 GROUP_MAX = int(os.environ.get("EXA_GROUP_MAX", "2"))
 ATTACH = os.environ.get("EXA_ATTACH", "1") == "1"  # light terms join heavy groups
 GROUP_RPT = int(os.environ.get("EXA_GROUP_RPT", "1"))  # records per thread of term groups (ILP)
+ATTACH_AUGS = os.environ.get("EXA_ATTACH_AUGS", "1") == "1"  # groups write aligned augments' J/H
 
 # Models with at most this many terms get a *specialised* module (metadata
 # compiled in as constants); larger ones (e.g. thousands of per-instance
@@ -325,12 +326,14 @@ class HostLayout:
                 if bk is not None:
                     lst = []
                     for (dd, rows, ent, rec) in bk:
+                        # (entry, record) int2 pairs: one 8-byte load per contribution;
+                        # kept writable until the blob is finalised (group attachment
+                        # below marks records whose J/H a term group writes: rec = -1)
+                        pairs = _i32(np.stack([ent, rec], axis=-1).reshape(-1), "bucket entries")
                         lst.append({
-                            "d": dd, "n": int(rows.size),
+                            "d": dd, "n": int(rows.size), "pairs": pairs,
                             "rows_off": i32.add(_i32(rows, "bucket rows")),
-                            # (entry, record) int2 pairs: one 8-byte load per contribution
-                            "pair_off": i32.add(_i32(np.stack([ent, rec], axis=-1).reshape(-1), "bucket entries"))
-                            if dd else -1,
+                            "pair_off": i32.add(pairs) if dd else -1,
                             "f_off": [f64.add(np.asarray(tp.reals[nm])[rows]) for nm in tp.tape.field_names],
                             "ix_off": [i32.add(_i32(np.asarray(tp.table.indices[nm])[rows], f"index column {nm!r}"))
                                        for nm in tp.tape.index_names],
@@ -351,14 +354,17 @@ class HostLayout:
             descs.append(d)
         self.descs = descs
         self.n_scr = scr
-        self.f64 = f64.array()
-        self.i32 = i32.array()
 
         # ---- term groups (specialised modules only) ---------------------------
         self.groups = []  # (pid, [term ids], members meta)
         self.group_of: dict = {}
+        self.group_augs: dict = {}  # group id -> [(aug term, record offset, member, slot)]
         if len(terms) <= META_CONST_MAX_TERMS and GROUP_MAX > 1:
             self._make_groups(terms, descs)
+            if ATTACH_AUGS:
+                self._attach_augs(terms)
+        self.f64 = f64.array()
+        self.i32 = i32.array()
 
         # ---- segments per callback -----------------------------------------
         segs = {m: [] for m in range(_lib.NMODES)}
@@ -559,6 +565,38 @@ class HostLayout:
             self.groups.append((self.term_pid[t0], grp, members))
             for t in grp:
                 self.group_of[t] = gi
+
+    def _attach_augs(self, terms):
+        """Bucketed augments (single-variable, field-free: pg, -p, -q ...) whose
+        records ``[off, off + n)`` gather, record for record, the same variable
+        as a slot of a term group over n records: the group thread writes
+        those records' J/H slots (coalesced, the variable already gathered)
+        instead of the row thread (scattered).  OPF: the -p/-q balance
+        augments of the from- and to-ends ride on the two flow groups."""
+        for gi, (_, grp, _) in enumerate(self.groups):
+            n = terms[grp[0]].nrec
+            slot_gids = []
+            for m, u in enumerate(grp):
+                for s_ in range(terms[u].tape.k):
+                    slot_gids.append((m, s_, np.asarray(terms[u].cols[s_], dtype=np.int64)))
+            for t, info in self.buckets.items():
+                for sel, u in enumerate(info["augs"]):
+                    a = terms[u]
+                    if a.nrec < n or a.nrec % n:
+                        continue
+                    gid = np.asarray(a.cols[0], dtype=np.int64)
+                    for off in range(0, a.nrec, n):
+                        if any(x[1] == off for x in self.group_augs.get(gi, []) if x[0] == u):
+                            continue
+                        hit = next(((m, s_) for (m, s_, g) in slot_gids if np.array_equal(g, gid[off:off + n])), None)
+                        if hit is None:
+                            continue
+                        self.group_augs.setdefault(gi, []).append((u, off, hit[0], hit[1]))
+                        for bk in info["buckets"]:  # the row thread no longer writes them
+                            pr = bk["pairs"].reshape(-1, 2)
+                            e, rc = pr[:, 0], pr[:, 1]
+                            mine = (e >= 0) & ((e >> BUCKET_GID_BITS) == sel) & (rc >= off) & (rc < off + n)
+                            rc[mine] = -1
 
     # accessors used by the specialised-kernel generator (jit.py)
     def term_descs(self):

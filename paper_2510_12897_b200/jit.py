@@ -351,7 +351,10 @@ def _specialised_kernels(layout) -> str:
   Hout[h0 + rec] = hv;
 }}""")
     for gid, (pid, grp, members) in enumerate(getattr(layout, "groups", [])):
-        out.append(group_source(gid, [(layout.patterns[layout.term_pid[u]], mem) for u, mem in zip(grp, members)]))
+        augs = [(layout.patterns[layout.term_pid[u]], off, m, s_)
+                for (u, off, m, s_) in getattr(layout, "group_augs", {}).get(gid, [])]
+        out.append(group_source(gid, [(layout.patterns[layout.term_pid[u]], mem) for u, mem in zip(grp, members)],
+                                augs))
     for m, name in enumerate(KERNEL_NAMES):
         for half, suffix in ((0, "_h"), (1, "_l")):
             out.append(_kernel_source(layout, m, half, name + suffix))
@@ -391,7 +394,7 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, full):
           f"      const double xv = __ldg(A.x + (e & {(1 << 29) - 1} & ~(e >> 31)));",
           f"      v = exa_bkval_T{t}(e, xv);"]
     if full:
-        L.append(f"      if (e >= 0) exa_bkout_T{t}(e, xv, wrow, rc, A);")  # (constant J/H: hoisted by the compiler)
+        L.append(f"      if (e >= 0 && rc >= 0) exa_bkout_T{t}(e, xv, wrow, rc, A);")
     L += ["    }",
           "    const int d = __popc(__ballot_sync(0xffffffffu, e >= 0));  // entries in lanes 1..d",
           "    double acc = lane == 0 ? 0.0 + v : v;",
@@ -466,7 +469,7 @@ def _kernel_source(layout, m, half, kname) -> str:
                 if full and early_out:
                     # x-independent augment J/H: stored while the gathers are in flight
                     for k in ks:
-                        cond = "" if k < always else f"if (e{k} >= 0) "
+                        cond = f"if (rc{k} >= 0) " if k < always else f"if (e{k} >= 0 && rc{k} >= 0) "
                         b_.append(f"    {cond}exa_bkout_T{t}(e{k}, 0.0, wrow, rc{k}, A);")
                 for k in ks:
                     b_.append(f"    const double v{k} = exa_bkval_T{t}(e{k}, xv{k});")
@@ -485,7 +488,7 @@ def _kernel_source(layout, m, half, kname) -> str:
                     else:
                         b_.append(f"    acc = e{k} >= 0 ? acc + v{k} : acc;")
                     if full and not early_out:
-                        cond = "" if k < always else f"if (e{k} >= 0) "
+                        cond = f"if (rc{k} >= 0) " if k < always else f"if (e{k} >= 0 && rc{k} >= 0) "
                         b_.append(f"    {cond}exa_bkout_T{t}(e{k}, xv{k}, wrow, rc{k}, A);")
             b_.append("    A.c[T.row_offset + r] = acc;")
             b_.append("    return;")
@@ -496,7 +499,10 @@ def _kernel_source(layout, m, half, kname) -> str:
             pid, grp, _ = layout.groups[t]
             for gm, u in enumerate(grp):
                 b_.append(f"    ExaTerm T{gm}; exa_init_T{u}(T{gm}, A);")
-            tl = ", ".join(f"T{gm}" for gm in range(len(grp)))
+            gaugs = getattr(layout, "group_augs", {}).get(t, [])
+            for k, (u, _, _, _) in enumerate(gaugs):
+                b_.append(f"    ExaTerm U{k}; exa_init_T{u}(U{k}, A);")
+            tl = ", ".join([f"T{gm}" for gm in range(len(grp))] + [f"U{k}" for k in range(len(gaugs))])
             rl = ", ".join(f"exa_rank(T{gm}, A)" for gm in range(len(grp)))
             if rpt == 1:
                 b_.append(f"    const int r = (b - {cta0}) * {threads} + tid;")

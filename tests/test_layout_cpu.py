@@ -67,9 +67,19 @@ def test_bucket_layout_reproduces_reference_row_order():
                 continue
             pairs = lay.i32[bk["pair_off"]:bk["pair_off"] + 2 * W * n]
             ent, rec = pairs[0::2], pairs[1::2]
-            assert np.array_equal(ent < 0, rec < 0)
+            assert np.all(rec[ent < 0] < 0)
             for sel, u in enumerate(info["augs"]):
-                seen[u].append(rec[(ent >= 0) & ((ent >> BUCKET_GID_BITS) == sel)])
+                r_ = rec[(ent >= 0) & ((ent >> BUCKET_GID_BITS) == sel)]
+                seen[u].append(r_[r_ >= 0])
+        # records whose J/H a term group writes instead (aligned augments)
+        for gi, lst in lay.group_augs.items():
+            n_g = lay.terms[lay.groups[gi][1][0]].nrec
+            for (u, off, m, s_) in lst:
+                if u in seen:
+                    seen[u].append(np.arange(off, off + n_g))
+                    # the group's slot gathers exactly the augment's variable
+                    g_term = lay.terms[lay.groups[gi][1][m]]
+                    assert np.array_equal(np.asarray(g_term.cols[s_]), np.asarray(lay.terms[u].cols[0])[off:off + n_g])
         for u, parts in seen.items():
             assert np.array_equal(np.sort(np.concatenate(parts)), np.arange(lay.terms[u].nrec))
 
