@@ -18,7 +18,7 @@ iw = hdr.index("Warp Stall Sampling (All Samples)")
 reasons = [(i, h[6:]) for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
 lines = []
 for r in rows[hi + 1:]:
-    if r and r[0]:
+    if r and r[0].isdigit():
         def f(i):
             try:
                 return float(r[i])
