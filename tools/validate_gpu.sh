@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round validation: GPU tests, smoke, bench (ours + reference arm), batched configs,
+# Round validation (run under gpurun): GPU tests, smoke, bench (ours + reference arm), batched configs,
 # ncu launch list + full capture of the set kernel (case13659) and of the N-1 set.
 TAG=${1:-r}
 mkdir -p gpurun_out
