@@ -463,6 +463,9 @@ def _kernel_source(layout, m, half, kname) -> str:
                     b_.append("    EXA_GRID_WAIT();")
                     if full:
                         b_.append("    const double wrow = __ldg(A.y + T.row_offset + r);")
+                    # base value first: its gathers issue with the entries' (a later
+                    # re-load behind the base J/H stores would cost a round trip)
+                    b_.append(f"    const double base = exa_val_{layout.term_pid[t]}(T, q, A, exa_rank(T, A));")
                 for k in ks:
                     # pad entries (-1) gather x[0]: branch-free, selected away below
                     b_.append(f"    const double xv{k} = __ldg(A.x + (e{k} & {(1 << 29) - 1} & ~(e{k} >> 31)));")
@@ -481,7 +484,7 @@ def _kernel_source(layout, m, half, kname) -> str:
                     if full and info["base_k"]:
                         b_.append(f"    exa_term_{layout.term_pid[t]}<EXA_M_JAC | EXA_M_HESS>(T, q, A, exa_rank(T, A), r);")
                     # reference order: zero-fill, base slice-add, augments in order (autodiff.py:573-580)
-                    b_.append(f"    double acc = 0.0 + exa_val_{layout.term_pid[t]}(T, q, A, exa_rank(T, A));")
+                    b_.append("    double acc = 0.0 + base;")
                 for k in ks:
                     if k < always:
                         b_.append(f"    acc = acc + v{k};")
