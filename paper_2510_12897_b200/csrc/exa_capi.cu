@@ -215,26 +215,44 @@ __global__ void exa_compress_reduce(int64_t nnz, const int64_t* __restrict__ ptr
 //   5 dual diagonal         delta_c != 0 ? 0 - delta_c : 0
 //   6 fixed row/col         0
 //   7 fixed diagonal        1
-__global__ void exa_kkt_kernel(int64_t n, const int2* __restrict__ desc, const double* __restrict__ h,
-                               const double* __restrict__ j, const double* __restrict__ sigma, double dw,
-                               double dc, double* __restrict__ out) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const int2 d = __ldg(desc + p);
+__device__ __forceinline__ double exa_kkt_entry(int2 d, const double* __restrict__ h, const double* __restrict__ j,
+                                                const double* __restrict__ sigma, double dw, double dc) {
   const int kind = (int)((unsigned)d.x >> 29);
   const int a = d.x & ((1 << 29) - 1);
-  double v;
   switch (kind) {
-    case 0: { const double hv = __ldg(h + a); v = (hv + 0.0) - 0.0; break; }
-    case 1: { const double hv = __ldg(h + a); v = (((hv + hv) - hv) + __ldg(sigma + d.y)) + dw; break; }
-    case 2: v = (0.0 + __ldg(sigma + d.y)) + dw; break;
-    case 3: v = __ldg(j + a); break;
-    case 4: v = -1.0; break;
-    case 5: v = dc != 0.0 ? 0.0 - dc : 0.0; break;
-    case 6: v = 0.0; break;
-    default: v = 1.0; break;
+    case 0: { const double hv = __ldg(h + a); return (hv + 0.0) - 0.0; }
+    case 1: { const double hv = __ldg(h + a); return (((hv + hv) - hv) + __ldg(sigma + d.y)) + dw; }
+    case 2: return (0.0 + __ldg(sigma + d.y)) + dw;
+    case 3: return __ldg(j + a);
+    case 4: return -1.0;
+    case 5: return dc != 0.0 ? 0.0 - dc : 0.0;
+    case 6: return 0.0;
+    default: return 1.0;
   }
-  out[p] = v;
+}
+
+// 4 entries per thread, strided by the grid so loads stay coalesced: all four
+// descriptors are loaded before any value gather (memory-level parallelism).
+__global__ void __launch_bounds__(256) exa_kkt_kernel(int64_t n, const int2* __restrict__ desc,
+                                                      const double* __restrict__ h, const double* __restrict__ j,
+                                                      const double* __restrict__ sigma, double dw, double dc,
+                                                      double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int2 d[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t p = p0 + u * stride;
+    d[u] = p < n ? __ldg(desc + p) : make_int2(6 << 29, 0);
+  }
+  double v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[u] = exa_kkt_entry(d[u], h, j, sigma, dw, dc);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t p = p0 + u * stride;
+    if (p < n) out[p] = v[u];
+  }
 }
 
 __global__ void exa_sincos_kernel(const double* __restrict__ x, double* __restrict__ s, double* __restrict__ c,
@@ -676,8 +694,8 @@ int exa_kkt_values(int64_t n, const int32_t* desc, const double* hvals, const do
   if (n < 0) return fail("exa_kkt_values: negative size");
   if (n == 0) return 0;
   if (!desc || !out || !sigma) return fail("exa_kkt_values: null argument");
-  exa_kkt_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, reinterpret_cast<const int2*>(desc), hvals, jvals,
-                                                                    sigma, delta_w, delta_c, out);
+  exa_kkt_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, (cudaStream_t)stream>>>(
+      n, reinterpret_cast<const int2*>(desc), hvals, jvals, sigma, delta_w, delta_c, out);
   CU(cudaGetLastError());
   return 0;
 }
