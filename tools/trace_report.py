@@ -15,7 +15,7 @@ dur = (c1 - c0) / 1965.0  # us at 1965 MHz
 # segment of each vb
 starts = segs[:, 2]
 sid = np.searchsorted(starts, vb, side="right") - 1
-kinds = {0: "term", 1: "row", 2: "fold", 3: "group", 4: "bkt"}
+kinds = {0: "term", 1: "row", 2: "fold", 3: "group", 4: "bkt", 5: "pair"}
 print("seg  term kind   nvb   warp-dur mean/max us   start min/max us   end max us")
 for s in range(len(segs)):
     m = ok & (sid == s)
