@@ -55,6 +55,8 @@ SINCOS_IMPL = os.environ.get("EXA_SINCOS_IMPL", "cr")  # "cuda" = libdevice sinc
 PERSIST = int(os.environ.get("EXA_PERSIST", "0"))
 TRACE = os.environ.get("EXA_TRACE", "0") == "1"  # per-warp timeline (diagnostics builds)
 BUCKET_EARLY_OUT = os.environ.get("EXA_BUCKET_EARLY_OUT", "0") == "1"  # experiment
+PREFETCH_XY = os.environ.get("EXA_PREFETCH_XY", "1") == "1"  # bulk L2 prefetch of x, y per set
+PREFETCH_CHUNK = int(os.environ.get("EXA_PREFETCH_CHUNK", "32768"))
 # Programmatic dependent launch: a CTA releases the next grid once its work is
 # issued; the next grid's CTAs load their (immutable) plan data before
 # griddepcontrol.wait, so back-to-back sets overlap one's drain with the next's
@@ -143,6 +145,23 @@ __shared__ long long exa_tp_s[EXA_TRACE_NT][4];
 #define EXA_TRACE_END(b, tid, nthreads) do {} while (0)
 #define EXA_TP(k, dep) do {} while (0)
 #endif
+"""
+
+_PREFETCH = r"""
+// Bulk L2 prefetch of the gathered inputs: CTA b < n prefetches chunk b of x
+// (then of y).  The first random gathers of a set would otherwise miss L2
+// (the previous set used other buffers) and go to DRAM one 32-B sector at a
+// time; a prefetch is only a read into L2, so issuing it before
+// griddepcontrol.wait is safe (L2 is the point of coherence).
+__device__ __forceinline__ void exa_prefetch_l2(const void* base, long long bytes, int chunk, int c) {
+  const long long off = (long long)c * chunk;
+  if (off >= bytes) return;
+  const char* p = reinterpret_cast<const char*>(base) + off;
+  long long len = bytes - off < chunk ? bytes - off : chunk;
+  len &= ~15LL;
+  if (len <= 0 || (reinterpret_cast<unsigned long long>(p) & 15)) return;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)len) : "memory");
+}
 """
 
 _COMMON = r"""
@@ -539,6 +558,17 @@ def _kernel_source(layout, m, half, kname) -> str:
     body = [f"extern \"C\" __global__ void __launch_bounds__({bounds}) {kname}(",
             "    const ExaTerm* __restrict__ terms, const ExaSeg* __restrict__ segs,",
             "    const int* __restrict__ cta_seg, ExaArgs A) {"]
+    # single-wave sets only (measured: +2% at case13659; batched sets, whose x
+    # and y are tens of MB, lose 3-4% to the extra L2 traffic)
+    if PREFETCH_XY and not V and threads == 32:
+        nvar, ncon = layout.plan.nvar, layout.plan.ncon
+        ch = PREFETCH_CHUNK
+        ncx = (8 * nvar + ch - 1) // ch
+        body.append(f"  if (threadIdx.x == 0 && blockIdx.x < {ncx}) exa_prefetch_l2(A.x, {8 * nvar}LL, {ch}, (int)blockIdx.x);")
+        if m in (0, 3):  # set / hess kernels gather multipliers too
+            ncy = (8 * ncon + ch - 1) // ch
+            body.append(f"  if (threadIdx.x == 0 && blockIdx.x >= {ncx} && blockIdx.x < {ncx + ncy}) "
+                        f"exa_prefetch_l2(A.y, {8 * ncon}LL, {ch}, (int)blockIdx.x - {ncx});")
     if V:
         body += [f"  const int tid = (int)threadIdx.x % {threads};",
                  f"  for (int b = (int)blockIdx.x + (int)gridDim.x * ((int)threadIdx.x / {threads}); b < {n_vb};"
@@ -586,6 +616,7 @@ def module_source(patterns, meta_const: bool = True, layout=None, threads: int =
     term_cases = "\n".join(
         f"    case {pc.pid}: exa_term_{pc.pid}<MODE>(T, r, A, rank); break;" for pc in patterns)
     val_cases = "\n".join(f"    case {pc.pid}: return exa_val_{pc.pid}(T, r, A, rank);" for pc in patterns)
+    parts.append(_PREFETCH)
     parts.append(_COMMON.replace("@TERM_CASES@", term_cases).replace("@VAL_CASES@", val_cases))
     if layout is None:
         parts.append(_KERNELS_GENERIC)
