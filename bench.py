@@ -400,7 +400,7 @@ def main():
             torch.distributed.destroy_process_group()
         return
     cpu = None
-    if not args.no_cpu_baseline and bps < 2e9:
+    if not args.no_cpu_baseline and bps < 2e9 and ws == 1:  # rank 0 at N=1 only
         xb, yb, wb = eval_inputs(model, 0)
         cpu = cpu_baseline(model, xb, yb, wb, args.cpu_seconds, args.workload)
     info = plans[0].info()
