@@ -185,7 +185,7 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "strong" if args.workload.startswith(("mp", "n1")) else "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.workload.startswith(("mp", "n1", "scen")) else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.workload, "sets_per_step": cores},
         "cpu_baseline": {"value": value, "unit": "sets/s", "cores": cores, "kind": "port",
                          "sample": f"{sets} sets ({cores} processes x {args.steps} steps) of "
@@ -225,7 +225,7 @@ def main():
 
     ws, rank, local = dist_setup()
     dev = torch.device("cuda", local)
-    sharded = args.workload.startswith(("mp", "n1"))
+    sharded = args.workload.startswith(("mp", "n1", "scen"))
     # batched configs: this rank's shard of ONE instance (strong scaling);
     # single-instance configs: every rank evaluates its own sets (weak scaling)
     model = build_workload(args.workload, lower_to_gpu=False, rank=rank, world=ws if sharded else 1)

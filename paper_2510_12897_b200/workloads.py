@@ -6,7 +6,10 @@ Configs:
 * ``case1354``    pglib case1354_pegase-shaped, polar, static;
 * ``case13659``   pglib case13659_pegase-shaped, polar, static (headline);
 * ``mp96_case1354``  96-period MPOPF with ramping on the 1354-shaped network;
-* ``n1_case2000``    N-1 batch on the case2000-shaped network (see :mod:`.scopf`).
+* ``n1_case2000``    N-1 batch on the case2000-shaped network (see :mod:`.scopf`);
+* ``scen96_case1354`` 96 independent load scenarios of the 1354-shaped network
+  (north_star "load scenarios": the multi-period builder without ramp rows,
+  ``corrective_action_ratio=None``, scenario load factors U(0.8, 1.2)).
 
 ``algorithmic_bytes`` is SURVEY §8(d)'s compulsory-traffic count for one
 callback set (cons + jac + hess): x and y once, every term parameter once
@@ -21,8 +24,12 @@ import numpy as np
 from .opf import mpopf_model, opf_model
 from .synth import demand_curve, pglib_shaped
 
-WORKLOADS = ("case14", "case1354", "case2000", "case13659", "mp96_case1354", "n1_case2000")
-SHARDED = ("mp", "n1")  # batched configs: one instance sharded over the ranks
+WORKLOADS = ("case14", "case1354", "case2000", "case13659", "mp96_case1354", "n1_case2000", "scen96_case1354")
+SHARDED = ("mp", "n1", "scen")  # batched configs: one instance sharded over the ranks
+
+
+def scenario_factors(S: int, seed: int = 7):
+    return np.random.default_rng(seed).uniform(0.8, 1.2, S)
 
 
 def _parse(name: str):
@@ -50,6 +57,14 @@ def build_workload(name: str, lower_to_gpu: bool = True, seed: int = 1, rank: in
         from .sharding import mpopf_shard
 
         return mpopf_shard(case, demand_curve(T), rank, world, 0.25, lower_to_gpu=lower_to_gpu).model
+    if head.startswith("scen"):
+        S = int(head[4:])
+        if world == 1:
+            return mpopf_model(case, scenario_factors(S), corrective_action_ratio=None, form="polar",
+                               lower_to_gpu=lower_to_gpu)[0]
+        from .sharding import mpopf_shard
+
+        return mpopf_shard(case, scenario_factors(S), rank, world, None, lower_to_gpu=lower_to_gpu).model
     if head.startswith("n1"):
         K = int(head[2:]) if len(head) > 2 else 1024
         from .scopf import instance_windows, scopf_model

@@ -40,7 +40,7 @@ def _gpu_set(model, x, y, w):
     return c, J, H
 
 
-@pytest.mark.parametrize("name", ["case1354", "case13659", "mp96_case1354"])
+@pytest.mark.parametrize("name", ["case1354", "case13659", "mp96_case1354", "scen96_case1354"])
 def test_set_parity_at_scale(name):
     model, (x, y, w) = workload(name)
     got = _gpu_set(model, x, y, w)
