@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define EXA_ABI_VERSION 3
+#define EXA_ABI_VERSION 4
 #define EXA_MAXF 16
 #define EXA_MAXI 16
 #define EXA_MAXK 16
@@ -117,6 +117,9 @@ typedef struct ExaPlanDesc {
   /* the module was built with programmatic-dependent-launch waits: launch
      with cudaLaunchAttributeProgrammaticStreamSerialization */
   int32_t pdl;
+  /* the module's set kernel offsets x, mult, c, jac, hess by blockIdx.y times
+     nvar, ncon, ncon, n_jac, n_hess (strided batches, exa_eval_set_batch) */
+  int32_t batchable;
 } ExaPlanDesc;
 
 /* ---- build-time: JIT ---------------------------------------------------- */
@@ -142,6 +145,14 @@ int exa_eval_hess(ExaPlan* plan, ExaWorkspace* ws, const double* x, const double
                   double obj_weight, double* hess, exa_stream_t stream);
 int exa_eval_set(ExaPlan* plan, ExaWorkspace* ws, const double* x, const double* mult,
                  double obj_weight, double* c, double* jac, double* hess, exa_stream_t stream);
+/* nsets independent callback sets of the same model in ONE launch (strided
+ * batch: set k reads x + k*nvar, mult + k*ncon and writes c + k*ncon,
+ * jac + k*n_jac, hess + k*n_hess; one obj_weight).  For throughput on
+ * independent evaluation points (scenario streams, multi-start, parallel
+ * trial points); each set's results are bitwise those of exa_eval_set.
+ * Plans with domain-checked operations or generic modules return an error. */
+int exa_eval_set_batch(ExaPlan* plan, ExaWorkspace* ws, int64_t nsets, const double* x, const double* mult,
+                       double obj_weight, double* c, double* jac, double* hess, exa_stream_t stream);
 /* exa_eval_set with HOST buffers (the reference-facing drop-in path: numpy
  * arrays in, numpy arrays out): copies x, mult to the workspace's device
  * staging, evaluates, copies c, jac, hess back -- all asynchronous on

@@ -16,7 +16,7 @@ MAXF = MAXI = MAXK = 16
 NMODES = 6
 NKERN = 12
 MODE_SET, MODE_CONS, MODE_JAC, MODE_HESS, MODE_OBJV, MODE_GRAD = range(6)
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 i64, i32, dbl, vp = C.c_int64, C.c_int32, C.c_double, C.c_void_p
 
@@ -49,7 +49,7 @@ class PlanDesc(C.Structure):
         ("grad_ptr", C.POINTER(i64)), ("grad_ent", C.POINTER(i64)), ("n_grad_ent", i64),
         ("cubin", vp), ("cubin_size", i64),
         ("has_domain_checks", i32),
-        ("persist", i32 * NKERN), ("pdl", i32),
+        ("persist", i32 * NKERN), ("pdl", i32), ("batchable", i32),
     ]
 
 
@@ -71,6 +71,7 @@ SIGNATURES = {
     "exa_eval_hess": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp]),
     "exa_eval_set": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp, vp, vp]),
     "exa_eval_set_host": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp, vp, vp]),
+    "exa_eval_set_batch": (C.c_int, [vp, vp, i64, vp, vp, dbl, vp, vp, vp, vp]),
     "exa_segment_sum": (C.c_int, [i64, vp, vp, vp, vp, vp]),
     "exa_kkt_values": (C.c_int, [i64, vp, vp, vp, vp, dbl, dbl, vp, vp]),
     "exa_domain_error": (C.c_int, [vp, vp, vp, C.POINTER(i64), C.POINTER(i32), C.POINTER(i64)]),

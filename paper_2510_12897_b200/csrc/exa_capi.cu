@@ -90,6 +90,7 @@ struct ExaPlan {
   int* cta_seg[EXA_NKERN] = {};
   int n_ctas[EXA_NKERN] = {};
   int persist[EXA_NKERN] = {};  /* virtual CTAs per real CTA (0 = classic grid) */
+  int batchable = 0;            /* module offsets x/y/c/J/H by blockIdx.y (exa_eval_set_batch) */
   int grid[EXA_NKERN] = {};     /* real CTAs launched */
   int n_segs_mode[EXA_NKERN] = {};
   int err_base[EXA_NMODES][2] = {};
@@ -401,6 +402,7 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
     const char* e = getenv("EXA_PDL");
     p->pdl = (d->pdl && !(e && e[0] == '0')) ? 1 : 0;
   }
+  p->batchable = d->batchable && !d->has_domain_checks;
   p->threads[0] = d->threads[0] > 0 ? d->threads[0] : 128;
   p->threads[1] = d->threads[1] > 0 ? d->threads[1] : 256;
   p->n_terms = d->n_terms;
@@ -533,7 +535,7 @@ int exa_plan_info(const ExaPlan* p, int64_t* bytes, int32_t* regs) {
   return 0;
 }
 
-static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStream_t st) {
+static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStream_t st, unsigned nbatch = 1) {
   A.seg_off = p->seg_off[kid];
   A.n_segs = p->n_segs_mode[kid];
   const ExaTerm* terms = p->terms;
@@ -544,7 +546,7 @@ static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStrea
   // previous work on the stream drains; it loads the (immutable) plan data,
   // then waits (griddepcontrol.wait) before touching caller buffers.
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p->grid[kid]);
+  cfg.gridDim = dim3(p->grid[kid], nbatch);
   cfg.blockDim = dim3(p->threads[kid & 1] * (p->persist[kid] ? p->persist[kid] : 1));
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
@@ -559,7 +561,7 @@ static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStrea
 
 // One callback = its heavy kernel on `st` and its light kernel on the
 // workspace's aux stream, forked/joined with events (graph-capturable).
-static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaStream_t st) {
+static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaStream_t st, unsigned nbatch = 1) {
   A.err = w->err;
   A.trace = g_trace;
   A.obj_base = p->err_base[mode][0];
@@ -574,14 +576,14 @@ static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaSt
     // light kernel's many short CTAs fill every SM
     CU(cudaEventRecord(w->fork, st));
     CU(cudaStreamWaitEvent(w->aux, w->fork, 0));
-    if ((rc = launch_kid(p, w, kh, A, st))) return rc;
-    if ((rc = launch_kid(p, w, kl, A, w->aux))) return rc;
+    if ((rc = launch_kid(p, w, kh, A, st, nbatch))) return rc;
+    if ((rc = launch_kid(p, w, kl, A, w->aux, nbatch))) return rc;
     CU(cudaEventRecord(w->join, w->aux));
     CU(cudaStreamWaitEvent(st, w->join, 0));
   } else if (h) {
-    rc = launch_kid(p, w, kh, A, st);
+    rc = launch_kid(p, w, kh, A, st, nbatch);
   } else if (l) {
-    rc = launch_kid(p, w, kl, A, st);
+    rc = launch_kid(p, w, kl, A, st, nbatch);
   }
   return rc;
 }
@@ -609,6 +611,22 @@ int exa_eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mu
   A.J = jac;
   A.H = hess;
   return launch_mode(p, w, EXA_MODE_SET, A, st);
+}
+
+int exa_eval_set_batch(ExaPlan* p, ExaWorkspace* ws, int64_t nsets, const double* x, const double* mult,
+                       double w_obj, double* c, double* jac, double* hess, exa_stream_t stream) {
+  if (!p) return fail("null plan");
+  if (nsets < 0 || nsets > 65535) return fail("exa_eval_set_batch: nsets %lld outside [0, 65535]", (long long)nsets);
+  if (!p->batchable) return fail("exa_eval_set_batch: this plan's module does not support batches");
+  if (nsets == 0) return 0;
+  EXA_PROLOGUE();
+  A.x = x;
+  A.y = mult;
+  A.w = w_obj;
+  A.c = c;
+  A.J = jac;
+  A.H = hess;
+  return launch_mode(p, w, EXA_MODE_SET, A, st, (unsigned)nsets);
 }
 
 int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,

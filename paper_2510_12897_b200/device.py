@@ -704,6 +704,7 @@ class DevicePlan:
             desc.n_ctas[m] = lay.n_ctas[m]
             desc.persist[m] = lay.persist[m]
         desc.pdl = int(lay.pdl)
+        desc.batchable = int(lay.specialised and not any(lay.persist))
         n_obj, n_con = len(plan.obj_terms), len(plan.con_terms)
         bases = {
             _lib.MODE_SET: (n_con, 0), _lib.MODE_CONS: (0, 0), _lib.MODE_JAC: (0, 0),

@@ -555,9 +555,14 @@ def _kernel_source(layout, m, half, kname) -> str:
         b_.append("  }")
         fn_body += b_
     fn_body.append("}")
+    plan = layout.plan
     body = [f"extern \"C\" __global__ void __launch_bounds__({bounds}) {kname}(",
             "    const ExaTerm* __restrict__ terms, const ExaSeg* __restrict__ segs,",
-            "    const int* __restrict__ cta_seg, ExaArgs A) {"]
+            "    const int* __restrict__ cta_seg, ExaArgs A) {",
+            # strided batches (exa_eval_set_batch): set blockIdx.y; 0 for single sets
+            "  { const long long k_ = blockIdx.y;",
+            f"    A.x += k_ * {plan.nvar}LL; A.y += k_ * {plan.ncon}LL; A.c += k_ * {plan.ncon}LL;",
+            f"    A.J += k_ * {plan.n_jac_slots}LL; A.H += k_ * {plan.n_hess_slots}LL; }}"]
     # single-wave sets only (measured: +2% at case13659; batched sets, whose x
     # and y are tens of MB, lose 3-4% to the extra L2 traffic)
     if PREFETCH_XY and not V and threads == 32:

@@ -250,3 +250,39 @@ def test_host_buffer_c_abi_matches_oracle(name):
         outs.append((hc.numpy().copy(), hJ.numpy().copy(), hH.numpy().copy()))
     for c, J, H in outs:
         assert bitwise_equal(c, c0) and bitwise_equal(J, J0) and bitwise_equal(H, H0)
+
+
+def test_strided_batch_equals_single_sets():
+    """exa_eval_set_batch: k independent sets in one launch, each bitwise equal
+    to its own exa_eval_set."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2510_12897_b200 import _lib
+    from paper_2510_12897_b200.workloads import build_workload, eval_inputs
+
+    model = build_workload("case1354")
+    dp = model.device_plan
+    lib = _lib.load()
+    S = 3
+    dev = torch.device("cuda", dp.device)
+    X = torch.stack([torch.from_numpy(eval_inputs(model, k)[0]) for k in range(S)]).to(dev)
+    Y = torch.stack([torch.from_numpy(eval_inputs(model, k)[1]) for k in range(S)]).to(dev)
+    nj, nh = model.plan.n_jac_slots, model.plan.n_hess_slots
+    Cb = torch.empty(S, model.ncon, dtype=torch.float64, device=dev)
+    Jb = torch.empty(S, nj, dtype=torch.float64, device=dev)
+    Hb = torch.empty(S, nh, dtype=torch.float64, device=dev)
+    st = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    _lib.check(lib.exa_eval_set_batch(dp.handle, None, S, X.data_ptr(), Y.data_ptr(), 0.5, Cb.data_ptr(),
+                                      Jb.data_ptr(), Hb.data_ptr(), st), "batch")
+    for k in range(S):
+        c = torch.empty(model.ncon, dtype=torch.float64, device=dev)
+        J = torch.empty(nj, dtype=torch.float64, device=dev)
+        H = torch.empty(nh, dtype=torch.float64, device=dev)
+        _lib.check(lib.exa_eval_set(dp.handle, None, X[k].data_ptr(), Y[k].data_ptr(), 0.5, c.data_ptr(),
+                                    J.data_ptr(), H.data_ptr(), st), "set")
+        torch.cuda.synchronize()
+        assert bitwise_equal(Cb[k].cpu().numpy(), c.cpu().numpy())
+        assert bitwise_equal(Jb[k].cpu().numpy(), J.cpu().numpy())
+        assert bitwise_equal(Hb[k].cpu().numpy(), H.cpu().numpy())
