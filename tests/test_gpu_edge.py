@@ -118,3 +118,49 @@ def test_domain_error_in_augment_row_sum():
     with pytest.raises(EvalDomainError) as exc:
         eval_constraints(model, np.array([1.0, -1.0, 2.0]), out)
     assert exc.value.op == "log" and exc.value.kind == "augment" and exc.value.record == 1
+
+
+def _bucket_model(n_rows=40, seed=3):
+    """Balance-like block with single-variable augments of two signs: rows
+    with 0, 1..8 and 9..31 contributions (every width class + warp rows),
+    a base term with a variable (J/H written by the row thread) and
+    duplicate variables across a row's augments."""
+    core = ModelCore()
+    x = core.add_variable(60, start=0.4)
+    y = core.add_variable(30, start=0.6)
+    rng = np.random.default_rng(seed)
+    base = core.add_constraint(-field("d") - field("g") * x["b"] * x["b"],
+                               DataTable({"d": rng.normal(size=n_rows), "g": rng.normal(size=n_rows),
+                                          "b": rng.integers(0, 60, n_rows)}))
+    counts = np.concatenate([[0, 0, 1, 2, 3, 5, 8, 9, 15, 31], rng.integers(0, 9, n_rows - 10)])
+    rows = np.repeat(np.arange(n_rows), counts)
+    rng.shuffle(rows)
+    half = rows.size // 2
+    core.modify_constraint(base, x["k"], DataTable({"k": rng.integers(0, 60, half), "row": base.row_offset + rows[:half]}))
+    core.modify_constraint(base, -y["m"], DataTable({"m": rng.integers(0, 30, rows.size - half),
+                                                    "row": base.row_offset + rows[half:]}))
+    return core
+
+
+def test_row_buckets_all_width_classes():
+    core = _bucket_model()
+    model = core.compile()
+    lay = model.device_plan.layout
+    assert lay.buckets, "expected the row-bucket layout"
+    widths = {bk["d"] for info in lay.buckets.values() for bk in info["buckets"]}
+    assert 32 in widths and 8 in widths and 0 in widths
+    _check_all(model)
+    _check_all(model, seed=5)
+
+
+def test_row_buckets_fall_back_to_folds():
+    """> 31 contributions in a row or > 4 distinct augments: warp folds /
+    serial rows, same results."""
+    core = ModelCore()
+    x = core.add_variable(80, start=0.3)
+    base = core.add_constraint(-field("d"), DataTable({"d": np.arange(6, dtype=float)}))
+    for a in range(5):  # five distinct augment terms
+        core.modify_constraint(base, x["k"] * (1.0 + a), DataTable({"k": np.arange(6) + a, "row": np.arange(6)}))
+    model = core.compile()
+    assert not model.device_plan.layout.buckets
+    _check_all(model)

@@ -100,3 +100,24 @@ def test_generic_module_compiles():
     lay = host_layout(model.plan)
     assert not lay.specialised
     assert precompile(model.plan)[:4] == b"\x7fELF"
+
+
+def test_bucket_layout_width_classes_and_fallbacks():
+    """Host replay of the bucket layout on a model with every width class and
+    warp rows; > 4 distinct augments -> no buckets."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from test_gpu_edge import _bucket_model
+
+    model = _bucket_model().compile(lower_to_gpu=False)
+    lay = host_layout(model.plan)
+    x = np.random.default_rng(2).uniform(0.2, 1.2, model.nvar)
+    ref = np.empty(model.ncon)
+    O.eval_constraints(model.plan, x, ref)
+    got = _bucket_cons(model, x)
+    rows = np.array(sorted(got))
+    assert rows.size == model.ncon
+    vals = np.array([got[r] for r in rows])
+    assert np.array_equal(vals, ref[rows]) and np.array_equal(np.signbit(vals), np.signbit(ref[rows]))
