@@ -755,15 +755,15 @@ def group_source(gid: int, entries: list, augs: list = ()) -> str:
                 pair = i * (i + 1) // 2 + j
                 dst = early if (const(col[i]) and not dup) else g.lines
                 dst.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
-    # attached augments (set kernel only): J/H of records off + r
-    SET = "(MODE == (EXA_M_CONS | EXA_M_JAC | EXA_M_HESS))"
+    # attached augments: their J slots in the jac/set kernels, H in hess/set
     aug_late = []
     for k, (apc, off, m, s_) in enumerate(augs):
         xs = vsyms[m][s_].name
-        post.append(f"  const double wa{k} = !{SET} ? 0.0 : __ldg(A.y + __ldg(U{k}.rows + {off} + r));")
+        post.append(f"  const double wa{k} = !(MODE & EXA_M_HESS) ? 0.0 : __ldg(A.y + __ldg(U{k}.rows + {off} + r));")
         dst = early if getattr(apc, "termx_const", False) else aug_late
-        dst.append(f"  if {SET} {{ double jv, hv; exa_termx_{apc.pid}({xs}, wa{k}, jv, hv); "
-                   f"Jout[U{k}.jac0 + {off}LL + r] = jv; Hout[U{k}.hess0 + {off}LL + r] = hv; }}")
+        dst.append(f"  if (MODE & (EXA_M_JAC | EXA_M_HESS)) {{ double jv, hv; exa_termx_{apc.pid}({xs}, wa{k}, jv, hv); "
+                   f"if (MODE & EXA_M_JAC) Jout[U{k}.jac0 + {off}LL + r] = jv; "
+                   f"if (MODE & EXA_M_HESS) Hout[U{k}.hess0 + {off}LL + r] = hv; }}")
     g.lines.extend(aug_late)
     args = ", ".join([f"const ExaTerm& T{m}" for m in range(M)] + [f"const ExaTerm& U{k}" for k in range(len(augs))])
     ranks = ", ".join(f"int rank{m}" for m in range(M))

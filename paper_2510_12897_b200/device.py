@@ -398,16 +398,18 @@ class HostLayout:
                 seg(_lib.MODE_SET, t, SEG_TERM, tp.nrec)
             if direct:
                 seg(_lib.MODE_CONS, t, SEG_TERM, tp.nrec)
-            if k or chk:
+            # bucketed blocks and their augments: the row threads write their
+            # J/H slots in the set, jac and hess kernels alike
+            if (k or chk) and t not in fused_set:
                 seg(_lib.MODE_JAC, t, SEG_TERM, tp.nrec)
-            if k:
+            if k and t not in fused_set:
                 seg(_lib.MODE_HESS, t, SEG_TERM, tp.nrec)
             if tp.kind == "constraint" and not direct:
                 if t in self.buckets:
                     for bi, bk in enumerate(self.buckets[t]["buckets"]):
                         nth = bk["n"] * (32 if bk["d"] == 32 else 1)  # long rows: a warp per row
-                        seg(_lib.MODE_SET, t, SEG_BUCKET + 16 * bi, nth)
-                        seg(_lib.MODE_CONS, t, SEG_BUCKET + 16 * bi, nth)
+                        for mode in (_lib.MODE_SET, _lib.MODE_CONS, _lib.MODE_JAC, _lib.MODE_HESS):
+                            seg(mode, t, SEG_BUCKET + 16 * bi, nth)
                 elif t in self.fold_slots:
                     seg(_lib.MODE_SET, t, SEG_FOLD, self.fold_slots[t])
                     seg(_lib.MODE_CONS, t, SEG_FOLD, self.fold_slots[t])

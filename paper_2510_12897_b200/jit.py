@@ -54,7 +54,6 @@ SINCOS_IMPL = os.environ.get("EXA_SINCOS_IMPL", "cr")  # "cuda" = libdevice sinc
 # assignment cannot balance the long flow CTAs).
 PERSIST = int(os.environ.get("EXA_PERSIST", "0"))
 TRACE = os.environ.get("EXA_TRACE", "0") == "1"  # per-warp timeline (diagnostics builds)
-BUCKET_EARLY_OUT = os.environ.get("EXA_BUCKET_EARLY_OUT", "0") == "1"  # experiment
 PREFETCH_XY = os.environ.get("EXA_PREFETCH_XY", "1") == "1"  # bulk L2 prefetch of x, y per set
 PREFETCH_CHUNK = int(os.environ.get("EXA_PREFETCH_CHUNK", "32768"))
 # Programmatic dependent launch: a CTA releases the next grid once its work is
@@ -358,7 +357,8 @@ def _specialised_kernels(layout) -> str:
             oc.append(f"{lab} exa_termx_{layout.term_pid[u]}(xv, w, jv, hv); j0 = {descs[u]['jac0']}LL;"
                       f" h0 = {descs[u]['hess0']}LL; break;")
         ocases = "\n".join(oc)
-        out.append(f"""__device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, const double w, const int rec, const ExaArgs& A) {{
+        out.append(f"""template <int WJ, int WH>
+__device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, const double w, const int rec, const ExaArgs& A) {{
   double jv, hv;
   long long j0, h0;
   switch ((unsigned)e >> 29) {{
@@ -366,8 +366,8 @@ def _specialised_kernels(layout) -> str:
   }}
   double* __restrict__ Jout = A.J;  // restrict: later gathers may be hoisted above these stores
   double* __restrict__ Hout = A.H;
-  Jout[j0 + rec] = jv;
-  Hout[h0 + rec] = hv;
+  if (WJ) Jout[j0 + rec] = jv;
+  if (WH) Hout[h0 + rec] = hv;
 }}""")
     for gid, (pid, grp, members) in enumerate(getattr(layout, "groups", [])):
         augs = [(layout.patterns[layout.term_pid[u]], off, m, s_)
@@ -380,14 +380,22 @@ def _specialised_kernels(layout) -> str:
     return "\n\n".join(out)
 
 
-def _warp_row_source(layout, t, bi, cta0, n_cta, threads, full):
+def _mode_outputs(m):
+    """(row value, J slots, H slots) a bucket segment produces in kernel m."""
+    return m in (0, 1), m in (0, 2), m in (0, 3)
+
+
+def _warp_row_source(layout, t, bi, cta0, n_cta, threads, m):
     """Long rows of a bucketed block: one warp per row.  Lane 0 evaluates the
     base term, lane l > 0 augment entry l-1; the row total is folded left to
     right through the lanes with shuffles -- ((0 + base) + a1) + a2 ... as the
-    reference's slice-add + np.add.at (autodiff.py:573-580)."""
+    reference's slice-add + np.add.at (autodiff.py:573-580).  In the jac /
+    hess kernels only the J / H slots of the base term and the augments."""
+    want_v, want_j, want_h = _mode_outputs(m)
     bk = layout.buckets[t]["buckets"][bi]
     n = bk["n"]
     pid = layout.term_pid[t]
+    base_mode = " | ".join(x for x, w in (("EXA_M_JAC", want_j), ("EXA_M_HESS", want_h)) if w)
     L = [f"  if (b < {cta0 + n_cta}) {{", f"    ExaTerm T; exa_init_T{t}(T, A);"]
     for i, off in enumerate(bk["f_off"]):
         L.append(f"    T.f[{i}] = A.f64 + {off}LL;")
@@ -398,32 +406,31 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, full):
           f"    if (q >= {n}) return;  // warp-uniform",
           f"    const int r = __ldg(A.i32 + {bk['rows_off']}LL + q);",
           f"    const int2 er = __ldg(reinterpret_cast<const int2*>(A.i32 + {bk['pair_off']}LL) + 32 * q + lane);",
-          "    const int e = er.x;"]
-    if full:
-        L.append("    const int rc = er.y;")
-    L.append("    EXA_GRID_WAIT();")
-    if full:
-        L.append("    const double wrow = __ldg(A.y + T.row_offset + r);")
-    L += ["    double v;",
-          "    if (lane == 0) {",
-          f"      v = exa_val_{pid}(T, q, A, exa_rank(T, A));"]
-    if full and layout.buckets[t]["base_k"]:
-        L.append(f"      exa_term_{pid}<EXA_M_JAC | EXA_M_HESS>(T, q, A, exa_rank(T, A), r);")
+          "    const int e = er.x, rc = er.y;",
+          "    EXA_GRID_WAIT();"]
+    L.append("    const double wrow = " + ("__ldg(A.y + T.row_offset + r);" if want_h else "0.0;"))
+    L += ["    double v = 0.0;",
+          "    if (lane == 0) {"]
+    if want_v:
+        L.append(f"      v = exa_val_{pid}(T, q, A, exa_rank(T, A));")
+    if base_mode and layout.buckets[t]["base_k"]:
+        L.append(f"      exa_term_{pid}<{base_mode}>(T, q, A, exa_rank(T, A), r);")
     L += ["    } else {",
-          f"      const double xv = __ldg(A.x + (e & {(1 << 29) - 1} & ~(e >> 31)));",
-          f"      v = exa_bkval_T{t}(e, xv);"]
-    if full:
-        L.append(f"      if (e >= 0 && rc >= 0) exa_bkout_T{t}(e, xv, wrow, rc, A);")
-    L += ["    }",
-          "    const int d = __popc(__ballot_sync(0xffffffffu, e >= 0));  // entries in lanes 1..d",
-          "    double acc = lane == 0 ? 0.0 + v : v;",
-          "    for (int s = 1; s <= d; ++s) {",
-          "      const double up = __shfl_up_sync(0xffffffffu, acc, 1);",
-          "      if (lane == s) acc = up + v;",
-          "    }",
-          "    if (lane == d) A.c[T.row_offset + r] = acc;",
-          "    return;",
-          "  }"]
+          f"      const double xv = __ldg(A.x + (e & {(1 << 29) - 1} & ~(e >> 31)));"]
+    if want_v:
+        L.append(f"      v = exa_bkval_T{t}(e, xv);")
+    if want_j or want_h:
+        L.append(f"      if (e >= 0 && rc >= 0) exa_bkout_T{t}<{int(want_j)}, {int(want_h)}>(e, xv, wrow, rc, A);")
+    L.append("    }")
+    if want_v:
+        L += ["    const int d = __popc(__ballot_sync(0xffffffffu, e >= 0));  // entries in lanes 1..d",
+              "    double acc = lane == 0 ? 0.0 + v : v;",
+              "    for (int s = 1; s <= d; ++s) {",
+              "      const double up = __shfl_up_sync(0xffffffffu, acc, 1);",
+              "      if (lane == s) acc = up + v;",
+              "    }",
+              "    if (lane == d) A.c[T.row_offset + r] = acc;"]
+    L += ["    return;", "  }"]
     return L
 
 
@@ -450,7 +457,7 @@ def _kernel_source(layout, m, half, kname) -> str:
         n_cta = (nrec + threads * rpt - 1) // (threads * rpt)
         b_ = [f"  if (b < {cta0 + n_cta}) {{"]
         if kind & 15 == 4 and layout.buckets[t]["buckets"][kind >> 4]["d"] == 32:
-            fn_body += _warp_row_source(layout, t, kind >> 4, cta0, n_cta, threads, m == 0)
+            fn_body += _warp_row_source(layout, t, kind >> 4, cta0, n_cta, threads, m)
             continue
         if kind & 15 == 4:  # row bucket of augment-target block t: one thread per row
             bk = layout.buckets[t]["buckets"][kind >> 4]
@@ -465,12 +472,13 @@ def _kernel_source(layout, m, half, kname) -> str:
             b_.append(f"    const int r = __ldg(A.i32 + {bk['rows_off']}LL + q);")
             # width class dd: entries k <= dd/2 always present, later ones may be -1
             always = dd // 2 + 1 if dd > 1 else dd
-            full = m == 0  # set kernel: also the base term's and the augments' J/H slots
+            # set kernel: row value, base term's and augments' J/H slots; cons:
+            # the value; jac / hess: only their slots
+            want_v, want_j, want_h = _mode_outputs(m)
             info = layout.buckets[t]
-            # (storing x-independent augment J/H before the gathers was measured
-            # slower: the scattered stores delay the row's gathers)
-            early_out = BUCKET_EARLY_OUT and all(getattr(layout.patterns[layout.term_pid[u]], "termx_const", False)
-                                                 for u in info["augs"])
+            need_x = want_v or not all(getattr(layout.patterns[layout.term_pid[u]], "termx_const", False)
+                                       for u in info["augs"])
+            base_mode = " | ".join(x for x, w in (("EXA_M_JAC", want_j), ("EXA_M_HESS", want_h)) if w)
             # chunks of 8 entries: loads, gathers (unconditional), in-order adds
             for c0 in range(0, max(dd, 1), 8):
                 ks = range(c0, min(dd, c0 + 8))
@@ -480,39 +488,38 @@ def _kernel_source(layout, m, half, kname) -> str:
                 if c0 == 0:
                     b_.append(f"    EXA_TP(0, {'e0' if dd else 'r'});")
                     b_.append("    EXA_GRID_WAIT();")
-                    if full:
-                        b_.append("    const double wrow = __ldg(A.y + T.row_offset + r);")
-                    # base value first: its gathers issue with the entries' (a later
-                    # re-load behind the base J/H stores would cost a round trip)
-                    b_.append(f"    const double base = exa_val_{layout.term_pid[t]}(T, q, A, exa_rank(T, A));")
+                    b_.append("    const double wrow = " + ("__ldg(A.y + T.row_offset + r);" if want_h else "0.0;"))
+                    if want_v:
+                        # base value first: its gathers issue with the entries' (a later
+                        # re-load behind the base J/H stores would cost a round trip)
+                        b_.append(f"    const double base = exa_val_{layout.term_pid[t]}(T, q, A, exa_rank(T, A));")
                 for k in ks:
                     # pad entries (-1) gather x[0]: branch-free, selected away below
-                    b_.append(f"    const double xv{k} = __ldg(A.x + (e{k} & {(1 << 29) - 1} & ~(e{k} >> 31)));")
-                if full and early_out:
-                    # x-independent augment J/H: stored while the gathers are in flight
-                    for k in ks:
-                        cond = f"if (rc{k} >= 0) " if k < always else f"if (e{k} >= 0 && rc{k} >= 0) "
-                        b_.append(f"    {cond}exa_bkout_T{t}(e{k}, 0.0, wrow, rc{k}, A);")
-                for k in ks:
-                    b_.append(f"    const double v{k} = exa_bkval_T{t}(e{k}, xv{k});")
+                    xv = f"__ldg(A.x + (e{k} & {(1 << 29) - 1} & ~(e{k} >> 31)))" if need_x else "0.0"
+                    b_.append(f"    const double xv{k} = {xv};")
+                    if want_v:
+                        b_.append(f"    const double v{k} = exa_bkval_T{t}(e{k}, xv{k});")
                 if c0 == 0:
-                    if ks:
+                    if ks and need_x:
                         b_.append("    EXA_TP(1, " + " + ".join(f"xv{k}" for k in ks) + ");")
                     # base term J/H after the entry gathers are issued (in-order issue:
                     # its stores wait on its own gather and would hold the others back)
-                    if full and info["base_k"]:
-                        b_.append(f"    exa_term_{layout.term_pid[t]}<EXA_M_JAC | EXA_M_HESS>(T, q, A, exa_rank(T, A), r);")
-                    # reference order: zero-fill, base slice-add, augments in order (autodiff.py:573-580)
-                    b_.append("    double acc = 0.0 + base;")
+                    if base_mode and info["base_k"]:
+                        b_.append(f"    exa_term_{layout.term_pid[t]}<{base_mode}>(T, q, A, exa_rank(T, A), r);")
+                    if want_v:
+                        # reference order: zero-fill, base slice-add, augments in order (autodiff.py:573-580)
+                        b_.append("    double acc = 0.0 + base;")
                 for k in ks:
-                    if k < always:
-                        b_.append(f"    acc = acc + v{k};")
-                    else:
-                        b_.append(f"    acc = e{k} >= 0 ? acc + v{k} : acc;")
-                    if full and not early_out:
+                    if want_v:
+                        if k < always:
+                            b_.append(f"    acc = acc + v{k};")
+                        else:
+                            b_.append(f"    acc = e{k} >= 0 ? acc + v{k} : acc;")
+                    if want_j or want_h:
                         cond = f"if (rc{k} >= 0) " if k < always else f"if (e{k} >= 0 && rc{k} >= 0) "
-                        b_.append(f"    {cond}exa_bkout_T{t}(e{k}, xv{k}, wrow, rc{k}, A);")
-            b_.append("    A.c[T.row_offset + r] = acc;")
+                        b_.append(f"    {cond}exa_bkout_T{t}<{int(want_j)}, {int(want_h)}>(e{k}, xv{k}, wrow, rc{k}, A);")
+            if want_v:
+                b_.append("    A.c[T.row_offset + r] = acc;")
             b_.append("    return;")
             b_.append("  }")
             fn_body += b_
