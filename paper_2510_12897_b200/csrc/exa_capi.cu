@@ -92,7 +92,6 @@ struct ExaPlan {
   int persist[EXA_NKERN] = {};  /* virtual CTAs per real CTA (0 = classic grid) */
   int batchable = 0;            /* module offsets x/y/c/J/H by blockIdx.y (exa_eval_set_batch) */
   int grid[EXA_NKERN] = {};     /* real CTAs launched */
-  int n_segs_mode[EXA_NKERN] = {};
   int err_base[EXA_NMODES][2] = {};
   int64_t n_vscr = 0, n_gscr = 0;
   int64_t* leaves = nullptr;
@@ -107,8 +106,6 @@ struct ExaPlan {
   ExaWorkspace* dflt = nullptr;
   size_t bytes = 0;
   int pdl = 0;
-  int seg_off[EXA_NKERN] = {};
-  bool meta_const = false;
 };
 
 // ---------------------------------------------------------------------------
@@ -447,7 +444,6 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
   for (int kid = 0; kid < EXA_NKERN; ++kid) {
     const int ns = d->n_segs[kid];
     const int th = p->threads[kid & 1];
-    p->n_segs_mode[kid] = ns;
     p->n_ctas[kid] = d->n_ctas[kid];
     if (ns == 0) continue;
     if ((rc = dev_upload(&p->segs[kid], reinterpret_cast<const ExaSeg*>(d->segs[kid]), (size_t)ns))) return bail(rc);
@@ -496,28 +492,6 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
       p->grid[kid] = need < occ * n_sm ? need : occ * n_sm;
     }
   }
-  // Constant-memory metadata variant: the module declares exa_terms_c /
-  // exa_segs_c; fill them with the term table and all callbacks' segments.
-  {
-    void* cterms = nullptr;
-    void* csegs = nullptr;
-    size_t nb_t = 0, nb_s = 0;
-    if (cudaLibraryGetGlobal(&cterms, &nb_t, p->lib, "exa_terms_c") == cudaSuccess &&
-        cudaLibraryGetGlobal(&csegs, &nb_s, p->lib, "exa_segs_c") == cudaSuccess) {
-      std::vector<ExaSeg> all;
-      for (int kid = 0; kid < EXA_NKERN; ++kid) {
-        p->seg_off[kid] = (int)all.size();
-        for (int s = 0; s < d->n_segs[kid]; ++s) all.push_back(reinterpret_cast<const ExaSeg*>(d->segs[kid])[s]);
-      }
-      if (terms.size() * sizeof(ExaTerm) > nb_t || all.size() * sizeof(ExaSeg) > nb_s)
-        return bail(fail("model too large for the constant-metadata module variant"));
-      CU(cudaMemcpy(cterms, terms.data(), terms.size() * sizeof(ExaTerm), cudaMemcpyHostToDevice));
-      if (!all.empty()) CU(cudaMemcpy(csegs, all.data(), all.size() * sizeof(ExaSeg), cudaMemcpyHostToDevice));
-      p->meta_const = true;
-    } else {
-      cudaGetLastError();  // clear the lookup failure
-    }
-  }
   if ((rc = ws_alloc(p, &p->dflt))) return bail(rc);
   *out = p;
   return 0;
@@ -536,8 +510,6 @@ int exa_plan_info(const ExaPlan* p, int64_t* bytes, int32_t* regs) {
 }
 
 static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStream_t st, unsigned nbatch = 1) {
-  A.seg_off = p->seg_off[kid];
-  A.n_segs = p->n_segs_mode[kid];
   const ExaTerm* terms = p->terms;
   const ExaSeg* segs = p->segs[kid];
   const int* cmap = p->cta_seg[kid];

@@ -30,9 +30,6 @@
 #define EXA_SEG_ROW 1  /* one thread per row, serial CSR loop (rows > 32 entries) */
 #define EXA_SEG_FOLD 2 /* warp-parallel row sums: one lane per contribution     */
 
-/* constant-memory metadata limits (models beyond them use global memory) */
-#define EXA_CMAX_TERMS 96
-#define EXA_CMAX_SEGS 1024
 
 typedef struct ExaTerm {
   const double* f[EXA_MAXF]; /* real field columns, normalised order     */
@@ -74,8 +71,6 @@ typedef struct ExaArgs {
   unsigned long long* err; /* domain-error key, atomicMin */
   int obj_base; /* domain-error rank offset of objective terms in this callback */
   int con_base; /* ... and of constraint-side terms */
-  int seg_off;  /* this callback's segments in the constant segment table */
-  int n_segs;
   const double* f64; /* plan blobs (model-specialised modules address terms */
   const int* i32;    /*   as blob + compile-time offsets)                    */
   long long* trace;  /* diagnostics timeline (EXA_TRACE modules), else 0 */

@@ -485,8 +485,8 @@ class HostLayout:
         # persistent kernels (specialised modules): PERSIST virtual CTAs per real CTA
         self.persist = [PERSIST if (self.specialised and self.n_ctas[kid]) else 0 for kid in range(_lib.NKERN)]
         self.pdl = PDL
-        self.source = module_source(self.patterns, meta_const=False,
-                                    layout=self if self.specialised else None, threads=self.threads[1])
+        self.source = module_source(self.patterns, layout=self if self.specialised else None,
+                                    threads=self.threads[1])
 
     def _make_groups(self, terms, descs):
         import hashlib

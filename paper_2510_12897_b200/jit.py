@@ -225,29 +225,13 @@ __device__ __forceinline__ void exa_rowfold(const ExaTerm& T, int slot, const Ex
 """
 
 _KERNELS_GENERIC = r"""
-// ---- metadata: constant memory (small models) or global memory -----------
-#if EXA_META_CONST
-__constant__ ExaTerm exa_terms_c[EXA_CMAX_TERMS];
-__constant__ ExaSeg exa_segs_c[EXA_CMAX_SEGS];
-#define EXA_TERM(i) exa_terms_c[(i)]
-#else
+// ---- metadata: run-time term / segment tables in global memory -----------
 #define EXA_TERM(i) terms[(i)]
-#endif
 
 template <int MODE>
 __device__ __forceinline__ void exa_kernel_body(const ExaTerm* __restrict__ terms, const ExaSeg* __restrict__ segs,
                                                 const int* __restrict__ cta_seg, const ExaArgs& A) {
-#if EXA_META_CONST
-  int lo = A.seg_off, hi = A.seg_off + A.n_segs - 1;
-  const int b = (int)blockIdx.x;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (exa_segs_c[mid].cta0 <= b) lo = mid; else hi = mid - 1;
-  }
-  const ExaSeg sg = exa_segs_c[lo];
-#else
   const ExaSeg sg = segs[__ldg(cta_seg + blockIdx.x)];
-#endif
   const int kind = sg.kind & 0xff, rpt = sg.kind >> 8;
   const ExaTerm& T = EXA_TERM(sg.term);
   auto val = [&](int t, int rec) -> double {
@@ -603,17 +587,15 @@ def _kernel_source(layout, m, half, kname) -> str:
 KERNEL_NAMES = ("exa_k_set", "exa_k_cons", "exa_k_jac", "exa_k_hess", "exa_k_objv", "exa_k_grad")
 
 
-def module_source(patterns, meta_const: bool = True, layout=None, threads: int = 32) -> str:
+def module_source(patterns, layout=None, threads: int = 32) -> str:
     """CUDA source of a model's module.
 
     ``layout`` given -> *model-specialised* module: term metadata and the
     CTA -> segment map are compiled in as constants (used for models with at
     most ``device.META_CONST_MAX_TERMS`` terms).  Otherwise a generic module
-    that reads the term/segment tables at run time, from constant memory when
-    ``meta_const`` or from global memory (very large term counts)."""
+    that reads the term/segment tables from global memory at run time."""
     seen: set = set()
     parts = ["// generated by paper_2510_12897_b200.jit",
-             f"#define EXA_META_CONST {1 if (meta_const and layout is None) else 0}",
              f"#define EXA_PDL {1 if PDL else 0}",
              f"#define EXA_PDL_EARLY {1 if PDL_EARLY else 0}",
              f"#define EXA_TRACE {1 if TRACE else 0}",
