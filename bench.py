@@ -426,6 +426,18 @@ def main():
         e2e_issue(i)
     e2e_sync()
     e2e_dt = time.perf_counter() - t0
+    # the drop-in Python call with numpy arrays (pageable host memory)
+    from paper_2510_12897_b200 import eval_callback_set
+
+    model.device_plan = plans[0]
+    xn, yn = xh.copy(), yh.copy()
+    cn, Jn, Hn = np.empty(model.ncon), np.empty(model.plan.n_jac_slots), np.empty(model.plan.n_hess_slots)
+    eval_callback_set(model, xn, yn, 1.0, cn, Jn, Hn)
+    t0 = time.perf_counter()
+    n_np = max(4, n_e2e // (2 * NS))
+    for _ in range(n_np):
+        eval_callback_set(model, xn, yn, 1.0, cn, Jn, Hn)
+    e2e_numpy = n_np / (time.perf_counter() - t0)
     # latency view: one set at a time, synchronised per set
     t0 = time.perf_counter()
     for i in range(n_e2e // NS):
@@ -474,7 +486,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": "sets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": (f"exa_eval_set_host (C ABI): pinned host x,y -> HBM -> set kernel -> pinned host c,J,H; "
                          f"one set per step, {NS} streams in round robin"),
-                "sequential_value": e2e_seq},
+                "sequential_value": e2e_seq, "numpy_api_value": e2e_numpy},
         "clocks": sampler.summary(),
         "batched": batched,
         "gpu_launches": args.steps * S,
