@@ -264,6 +264,24 @@ def eval_callback_set(model, x, mult, obj_weight: float, out_c, out_jac, out_hes
     st.finish()
 
 
+def eval_callback_set_batch(model, X, Y, obj_weight: float, C_out, J_out, H_out) -> None:
+    """k independent callback sets in ONE launch: row i of the (k, n) CUDA
+    tensors X, Y, C_out, J_out, H_out is one set (``exa_eval_set_batch``);
+    each row's results are bitwise those of :func:`eval_callback_set`."""
+    torch = _torch()
+    plan = model.plan
+    k = int(X.shape[0]) if getattr(X, "ndim", 0) == 2 else -1
+    for a, n, what in ((X, model.nvar, "X"), (Y, model.ncon, "Y"), (C_out, model.ncon, "C_out"),
+                       (J_out, plan.n_jac_slots, "J_out"), (H_out, plan.n_hess_slots, "H_out")):
+        if not _is_cuda(a) or a.dtype != torch.float64 or not a.is_contiguous() or tuple(a.shape) != (k, n):
+            raise ValueError(f"{what} must be a contiguous float64 CUDA tensor of shape ({k}, {n})")
+    dp = _dplan(model)
+    s = C.c_void_p(torch.cuda.current_stream(X.device).cuda_stream)
+    _lib.check(dp._lib.exa_eval_set_batch(dp.handle, None, k, X.data_ptr(), Y.data_ptr(), float(obj_weight),
+                                          C_out.data_ptr(), J_out.data_ptr(), H_out.data_ptr(), s),
+               "eval_set_batch")
+
+
 @dataclass(eq=False)
 class CompressedPattern:
     """Deduplicated COO plus the raw-slot -> compressed-slot map

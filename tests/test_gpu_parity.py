@@ -274,8 +274,9 @@ def test_strided_batch_equals_single_sets():
     Jb = torch.empty(S, nj, dtype=torch.float64, device=dev)
     Hb = torch.empty(S, nh, dtype=torch.float64, device=dev)
     st = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
-    _lib.check(lib.exa_eval_set_batch(dp.handle, None, S, X.data_ptr(), Y.data_ptr(), 0.5, Cb.data_ptr(),
-                                      Jb.data_ptr(), Hb.data_ptr(), st), "batch")
+    from paper_2510_12897_b200 import eval_callback_set_batch
+
+    eval_callback_set_batch(model, X, Y, 0.5, Cb, Jb, Hb)
     for k in range(S):
         c = torch.empty(model.ncon, dtype=torch.float64, device=dev)
         J = torch.empty(nj, dtype=torch.float64, device=dev)
