@@ -38,8 +38,19 @@ import os
 import numpy as np
 
 _SIN_COS = ("sin", "cos")
-# EXA_EXACT_ZERO_SIGN=1 keeps every 0 + x of the reference (bitwise identical
-# signs of zero in J/H); default drops them in derivative space (see Gen.bin)
+
+
+def _zero_const(v) -> bool:
+    """A generation-time constant 0 (structural zero of a derivative)."""
+    if isinstance(v, Sym):
+        return False
+    return float(v.value if isinstance(v, Arr) else v) == 0.0
+
+
+# EXA_EXACT_ZERO_SIGN=1 keeps every 0 + x of the reference and the sign of the
+# structural zeros w * 0 (bitwise identical signs of zero in J/H); the default
+# drops the former in derivative space (see Gen.bin) and writes the latter as
+# +0.0 without loading the weight -- IEEE-equal values either way
 _DERIV_ZERO_ELISION = os.environ.get("EXA_EXACT_ZERO_SIGN", "0") != "1"
 
 
@@ -611,7 +622,10 @@ class PatternCode:
                     bi, bj = self.slot_struct[i][0], self.slot_struct[j][0]
                     if i != j and bi == bj:
                         expr = f"(c{i} == c{j} ? {expr} * 2.0 : {expr})"
-                    out.append(f"      Hout[T.hess0 + {pair}LL * T.nrec + o] = wgt * {expr};")
+                    if _DERIV_ZERO_ELISION and _zero_const(val):
+                        out.append(f"      Hout[T.hess0 + {pair}LL * T.nrec + o] = 0.0;  // structural zero")
+                    else:
+                        out.append(f"      Hout[T.hess0 + {pair}LL * T.nrec + o] = wgt * {expr};")
                     pair += 1
             out.append("    }")
             out.append("  }")
@@ -638,10 +652,13 @@ class PatternCode:
             # x-independent J/H (pg, -p, ...: +-1 and w * 0): row buckets store
             # them before gathering the variable
             self.termx_const = not isinstance(gradx[0], Sym) and not isinstance(colx[0], Sym)
+            # Hessian entry is the structural zero w * 0 (pg, -p, ...)
+            self.termx_hzero = not isinstance(colx[0], Sym) and float(
+                colx[0].value if isinstance(colx[0], Arr) else colx[0]) == 0.0
             out.append(f"__device__ __forceinline__ void exa_termx_{pid}(const double x0, const double wgt, double& jv, double& hv) {{")
             out.extend(gx.lines)
             out.append(f"  jv = {R(gradx[0])};")
-            out.append(f"  hv = wgt * {R(colx[0])};")
+            out.append("  hv = 0.0;" if (_DERIV_ZERO_ELISION and _zero_const(colx[0])) else f"  hv = wgt * {R(colx[0])};")
             out.append("}")
         # records per thread: light patterns amortise per-thread overheads and
         # overlap several records' loads; heavy ones keep one record per thread
@@ -753,13 +770,22 @@ def group_source(gid: int, entries: list, augs: list = ()) -> str:
                 if dup:
                     expr = f"({cnames[m][i]} == {cnames[m][j]} ? {expr} * 2.0 : {expr})"
                 pair = i * (i + 1) // 2 + j
+                if _DERIV_ZERO_ELISION and _zero_const(col[i]):  # structural zero: +0.0, no weight
+                    early.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = 0.0;")
+                    continue
                 dst = early if (const(col[i]) and not dup) else g.lines
                 dst.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
     # attached augments: their J slots in the jac/set kernels, H in hess/set
     aug_late = []
     for k, (apc, off, m, s_) in enumerate(augs):
         xs = vsyms[m][s_].name
-        post.append(f"  const double wa{k} = !(MODE & EXA_M_HESS) ? 0.0 : __ldg(A.y + __ldg(U{k}.rows + {off} + r));")
+        if _DERIV_ZERO_ELISION and getattr(apc, "termx_hzero", False):
+            # structural-zero Hessian entry: written as +0.0 (the reference's
+            # w * 0.0 carries the multiplier's sign; IEEE-equal, see the zero-sign
+            # relaxation) -- saves a two-load chain per record
+            post.append(f"  const double wa{k} = 0.0;")
+        else:
+            post.append(f"  const double wa{k} = !(MODE & EXA_M_HESS) ? 0.0 : __ldg(A.y + __ldg(U{k}.rows + {off} + r));")
         dst = early if getattr(apc, "termx_const", False) else aug_late
         dst.append(f"  if (MODE & (EXA_M_JAC | EXA_M_HESS)) {{ double jv, hv; exa_termx_{apc.pid}({xs}, wa{k}, jv, hv); "
                    f"if (MODE & EXA_M_JAC) Jout[U{k}.jac0 + {off}LL + r] = jv; "

@@ -6,6 +6,7 @@ last launch's records (SM, virtual CTA, clock64 and globaltimer start/end).
 """
 import ctypes as C
 import os
+import os
 import sys
 from pathlib import Path
 
@@ -21,7 +22,7 @@ assert jit.TRACE, "set EXA_TRACE=1"
 name = sys.argv[1]
 out = sys.argv[2]
 model = build_workload(name, lower_to_gpu=False)
-R = 11
+R = int(os.environ.get("EXA_R", "11"))
 dev = torch.device("cuda", 0)
 plans = [DevicePlan(model, 0) for _ in range(R)]
 lay = plans[0].layout
