@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define EXA_ABI_VERSION 4
+#define EXA_ABI_VERSION 5
 #define EXA_MAXF 16
 #define EXA_MAXI 16
 #define EXA_MAXK 16
@@ -120,6 +120,13 @@ typedef struct ExaPlanDesc {
   /* the module's set kernel offsets x, mult, c, jac, hess by blockIdx.y times
      nvar, ncon, ncon, n_jac, n_hess (strided batches, exa_eval_set_batch) */
   int32_t batchable;
+  /* host path (exa_eval_set_host): raw J / H slot runs whose value is the same
+     constant for every record and call, int64 triples (first slot, length,
+     IEEE-754 bits of the value): the first n_fill_jac index J, the next
+     n_fill_hess index H, sorted and disjoint.  They are filled on the host
+     instead of being copied from the device.  May be null / 0. */
+  const int64_t* host_fill;
+  int32_t n_fill_jac, n_fill_hess;
 } ExaPlanDesc;
 
 /* ---- build-time: JIT ---------------------------------------------------- */
@@ -155,10 +162,13 @@ int exa_eval_set_batch(ExaPlan* plan, ExaWorkspace* ws, int64_t nsets, const dou
                        double obj_weight, double* c, double* jac, double* hess, exa_stream_t stream);
 /* exa_eval_set with HOST buffers (the reference-facing drop-in path: numpy
  * arrays in, numpy arrays out): copies x, mult to the workspace's device
- * staging, evaluates, copies c, jac, hess back -- all asynchronous on
- * `stream` (synchronise it before reading the outputs).  Pinned host memory
- * makes the copies asynchronous, so sets on distinct workspaces and streams
- * overlap their H2D copy, kernel and D2H copy. */
+ * staging, evaluates, copies c and the x-dependent J/H ranges back -- all
+ * asynchronous on `stream` (synchronise it before reading the outputs; a
+ * non-legacy stream gets one batched D2H call) -- and writes the plan's
+ * constant J/H runs (ExaPlanDesc.host_fill) into jac/hess with host threads
+ * before returning.  Pinned host memory makes the copies asynchronous, so
+ * sets on distinct workspaces and streams overlap their H2D copy, kernel and
+ * D2H copy. */
 int exa_eval_set_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, const double* mult_host,
                       double obj_weight, double* c_host, double* jac_host, double* hess_host,
                       exa_stream_t stream);

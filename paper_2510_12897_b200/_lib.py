@@ -16,7 +16,7 @@ MAXF = MAXI = MAXK = 16
 NMODES = 6
 NKERN = 12
 MODE_SET, MODE_CONS, MODE_JAC, MODE_HESS, MODE_OBJV, MODE_GRAD = range(6)
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 i64, i32, dbl, vp = C.c_int64, C.c_int32, C.c_double, C.c_void_p
 
@@ -49,7 +49,7 @@ class PlanDesc(C.Structure):
         ("grad_ptr", C.POINTER(i64)), ("grad_ent", C.POINTER(i64)), ("n_grad_ent", i64),
         ("cubin", vp), ("cubin_size", i64),
         ("has_domain_checks", i32),
-        ("persist", i32 * NKERN), ("pdl", i32), ("batchable", i32),
+        ("persist", i32 * NKERN), ("pdl", i32), ("batchable", i32), ("host_fill", C.POINTER(C.c_int64)), ("n_fill_jac", i32), ("n_fill_hess", i32),
     ]
 
 

@@ -252,6 +252,20 @@ def eval_callback_set(model, x, mult, obj_weight: float, out_c, out_jac, out_hes
         if _shape(buf) != (n,):
             raise ValueError(f"{what} buffer has shape {_shape(buf)}, expected ({n},)")
     dp = _dplan(model)
+    bufs = (x, mult, out_c, out_jac, out_hess)
+    if all(isinstance(b, np.ndarray) and b.dtype == np.float64 and b.flags.c_contiguous for b in bufs) \
+            and all(b.flags.writeable for b in bufs[2:]):
+        # all-numpy call: the C ABI host path (H2D, set kernel, D2H of the
+        # x-dependent ranges straight into the caller's arrays, constant runs
+        # filled on the host)
+        torch = _torch()
+        s = C.c_void_p(torch.cuda.current_stream(torch.device("cuda", dp.device)).cuda_stream)
+        ptr = [b.ctypes.data if b.size else 0 for b in bufs]
+        _lib.check(dp._lib.exa_eval_set_host(dp.handle, None, ptr[0], ptr[1], float(obj_weight), ptr[2], ptr[3],
+                                             ptr[4], s), "eval_set_host")
+        _raise_domain(dp, s, "set")
+        torch.cuda.current_stream(torch.device("cuda", dp.device)).synchronize()
+        return
     st = _Stage(dp)
     xp = st.inp(x)
     yp = st.inp(mult) if model.ncon else 0

@@ -567,6 +567,20 @@ class PatternCode:
             by_seed.append(self._slot_sums(g, self._adjoint_tangents(g, v, adj, t)))
         body_grad = g.lines[n_value_lines:n_grad_lines]
         body_hess = g.lines[n_grad_lines:]
+        # x- and y-independent outputs (every record, every call): constant J
+        # slots and, under the zero-sign relaxation, the structural-zero
+        # Hessian pairs (written as +0.0).  The host path fills these into the
+        # caller's arrays instead of copying them over PCIe (exa_eval_set_host).
+        self.jconst = {s: float(grads[s].value if isinstance(grads[s], Arr) else grads[s])
+                       for s in range(k) if not isinstance(grads[s], Sym)}
+        self.hzero = []
+        if _DERIV_ZERO_ELISION:
+            pair = 0
+            for i in range(k):
+                for j in range(i + 1):
+                    if _zero_const(by_seed[j][i]):
+                        self.hzero.append(pair)
+                    pair += 1
 
         out = []
         pid = self.pid

@@ -17,8 +17,13 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/exa.h"
@@ -106,6 +111,11 @@ struct ExaPlan {
   ExaWorkspace* dflt = nullptr;
   size_t bytes = 0;
   int pdl = 0;
+  /* host path: constant runs filled on the host, (first, length, value) */
+  struct Run { int64_t a, n; double v; };
+  std::vector<Run> fill_jac, fill_hess;
+  /* ... and the complementary slot ranges copied D2H, (first, length) */
+  std::vector<std::pair<int64_t, int64_t>> copy_jac, copy_hess;
 };
 
 // ---------------------------------------------------------------------------
@@ -400,6 +410,27 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
     p->pdl = (d->pdl && !(e && e[0] == '0')) ? 1 : 0;
   }
   p->batchable = d->batchable && !d->has_domain_checks;
+  {
+    auto take = [&](const int64_t* tr, int n, int64_t total, std::vector<ExaPlan::Run>& fill,
+                    std::vector<std::pair<int64_t, int64_t>>& copy) -> int {
+      int64_t at = 0;
+      for (int i = 0; i < n; ++i) {
+        const int64_t a = tr[3 * i], len = tr[3 * i + 1];
+        double v;
+        std::memcpy(&v, &tr[3 * i + 2], sizeof v);
+        if (a < at || len <= 0 || a + len > total) return fail("host_fill: runs must be sorted, disjoint, in range");
+        if (a > at) copy.push_back({at, a - at});
+        fill.push_back({a, len, v});
+        at = a + len;
+      }
+      if (at < total) copy.push_back({at, total - at});
+      return 0;
+    };
+    const int nj = d->host_fill ? d->n_fill_jac : 0, nh = d->host_fill ? d->n_fill_hess : 0;
+    if ((rc = take(d->host_fill, nj, d->n_jac, p->fill_jac, p->copy_jac))) return bail(rc);
+    if ((rc = take(d->host_fill ? d->host_fill + 3 * nj : nullptr, nh, d->n_hess, p->fill_hess, p->copy_hess)))
+      return bail(rc);
+  }
   p->threads[0] = d->threads[0] > 0 ? d->threads[0] : 128;
   p->threads[1] = d->threads[1] > 0 ? d->threads[1] : 256;
   p->n_terms = d->n_terms;
@@ -601,6 +632,98 @@ int exa_eval_set_batch(ExaPlan* p, ExaWorkspace* ws, int64_t nsets, const double
   return launch_mode(p, w, EXA_MODE_SET, A, st, (unsigned)nsets);
 }
 
+// ---------------------------------------------------------------------------
+// host fill of constant output runs: a small persistent pool of threads (the
+// caller included) writes the runs in 256 KB pieces; a run of +0.0 is a memset
+// ---------------------------------------------------------------------------
+namespace {
+struct FillPool {
+  struct Piece { double* dst; int64_t n; double v; };
+  std::mutex call_mu;  // one fill at a time
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<std::thread> workers;
+  const std::vector<Piece>* job = nullptr;
+  uint64_t gen = 0;
+  std::atomic<size_t> next{0};
+  std::atomic<int> active{0};
+
+  static void run(const Piece& q) {
+    if (q.v == 0.0 && !std::signbit(q.v)) {
+      std::memset(q.dst, 0, q.n * sizeof(double));
+    } else {
+      for (int64_t i = 0; i < q.n; ++i) q.dst[i] = q.v;
+    }
+  }
+  void drain(const std::vector<Piece>& pcs) {
+    for (size_t i; (i = next.fetch_add(1)) < pcs.size();) run(pcs[i]);
+  }
+  explicit FillPool(int n) {
+    for (int t = 0; t < n; ++t)
+      workers.emplace_back([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          const std::vector<Piece>* j;
+          {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return gen != seen; });
+            seen = gen;
+            j = job;
+            active.fetch_add(1);
+          }
+          if (j) drain(*j);
+          active.fetch_sub(1);
+        }
+      });
+    for (auto& t : workers) t.detach();
+  }
+  void fill(const std::vector<Piece>& pcs) {
+    std::lock_guard<std::mutex> g(call_mu);
+    int64_t bytes = 0;
+    for (auto& q : pcs) bytes += q.n * 8;
+    next.store(0);
+    if (!workers.empty() && bytes > (1 << 20)) {
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        job = &pcs;
+        ++gen;
+      }
+      cv.notify_all();
+      drain(pcs);
+      // every piece is claimed; wait for the workers still writing one
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        job = nullptr;
+      }
+      while (active.load() > 0) std::this_thread::yield();
+    } else {
+      drain(pcs);
+    }
+  }
+};
+
+FillPool& fill_pool() {
+  static FillPool* pool = [] {
+    int n = (int)std::thread::hardware_concurrency() / 2;
+    if (const char* e = std::getenv("EXA_HOST_FILL_THREADS")) n = std::atoi(e);
+    if (n > 8) n = 8;
+    return new FillPool(n > 0 ? n - 1 : 0);  // the caller is the n-th
+  }();
+  return *pool;
+}
+}  // namespace
+
+static void host_fill(const ExaPlan* p, double* jac, double* hess) {
+  constexpr int64_t kPiece = 32768;  // doubles (256 KB)
+  std::vector<FillPool::Piece> pcs;
+  for (auto* rs : {&p->fill_jac, &p->fill_hess}) {
+    double* out = rs == &p->fill_jac ? jac : hess;
+    for (auto& r : *rs)
+      for (int64_t o = 0; o < r.n; o += kPiece) pcs.push_back({out + r.a + o, r.n - o < kPiece ? r.n - o : kPiece, r.v});
+  }
+  if (!pcs.empty()) fill_pool().fill(pcs);
+}
+
 int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
                       double* jac, double* hess, exa_stream_t stream) {
   if (!p) return fail("null plan");
@@ -617,9 +740,29 @@ int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const doubl
   if (p->nvar) CU(cudaMemcpyAsync(w->dx, x, p->nvar * sizeof(double), cudaMemcpyHostToDevice, st));
   if (p->ncon) CU(cudaMemcpyAsync(w->dy, mult, p->ncon * sizeof(double), cudaMemcpyHostToDevice, st));
   if (int rc = exa_eval_set(p, w, w->dx, w->dy, w_obj, w->dc, w->dJ, w->dH, stream)) return rc;
-  if (p->ncon) CU(cudaMemcpyAsync(c, w->dc, p->ncon * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (p->n_jac) CU(cudaMemcpyAsync(jac, w->dJ, p->n_jac * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (p->n_hess) CU(cudaMemcpyAsync(hess, w->dH, p->n_hess * sizeof(double), cudaMemcpyDeviceToHost, st));
+  // D2H of everything but the constant runs (one batched call on a real
+  // stream), then the constant runs written on the host while the DMA runs
+  std::vector<void*> dst, src;
+  std::vector<size_t> len;
+  if (p->ncon) { dst.push_back(c); src.push_back(w->dc); len.push_back(p->ncon * sizeof(double)); }
+  for (auto& r : p->copy_jac) {
+    dst.push_back(jac + r.first); src.push_back(w->dJ + r.first); len.push_back(r.second * sizeof(double));
+  }
+  for (auto& r : p->copy_hess) {
+    dst.push_back(hess + r.first); src.push_back(w->dH + r.first); len.push_back(r.second * sizeof(double));
+  }
+  if (!dst.empty()) {
+    if (st != nullptr && st != cudaStreamLegacy && st != cudaStreamPerThread) {
+      cudaMemcpyAttributes at = {};
+      at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+      size_t ai = 0, fidx = 0;
+      CU(cudaMemcpyBatchAsync(dst.data(), src.data(), len.data(), dst.size(), &at, &ai, 1, &fidx, st));
+    } else {
+      for (size_t i = 0; i < dst.size(); ++i) CU(cudaMemcpyAsync(dst[i], src[i], len[i], cudaMemcpyDeviceToHost, st));
+    }
+  }
+  host_fill(p, jac, hess);
   return 0;
 }
 

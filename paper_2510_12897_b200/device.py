@@ -479,6 +479,7 @@ class HostLayout:
         self.leaves = np.array(leaves, dtype=np.int64).reshape(-1, 2)
         self.prog = np.array(prog, dtype=np.int64).reshape(-1, 3)
         self.grad_ptr, self.grad_ent = self._grad_csr(plan.nvar)
+        self.fill_jac, self.fill_hess = self._host_fill(terms)
 
         # ---- module source ---------------------------------------------------
         self.specialised = len(terms) <= META_CONST_MAX_TERMS
@@ -610,6 +611,36 @@ class HostLayout:
     def mode_segments(self, m):
         return self.segs[m]
 
+    def _host_fill(self, terms):
+        """Runs of raw J / H slots whose value is the same constant for every
+        record and every call (constant Jacobian slots; structural-zero Hessian
+        pairs, +0.0 under the zero-sign relaxation) as int64 triples (first
+        slot, length, value bits), adjacent equal runs merged.  The host path
+        fills them into the caller's arrays and copies only the rest over
+        PCIe; the kernels still write them (device callers get every slot)."""
+        runs_j, runs_h = [], []
+        for t, tp in enumerate(terms):
+            pc = self.patterns[self.term_pid[t]]
+            d, n = self.descs[t], tp.nrec
+            if n == 0 or not pc.k:
+                continue
+            if tp.kind != "objective":
+                for s_, v in pc.jconst.items():
+                    runs_j.append((d["jac0"] + s_ * n, n, int(np.float64(v).view(np.int64))))
+            for pr in pc.hzero:
+                runs_h.append((d["hess0"] + pr * n, n, 0))
+
+        def merge(runs):
+            out = []
+            for a, n, v in sorted(runs):
+                if out and out[-1][0] + out[-1][1] == a and out[-1][2] == v:
+                    out[-1][1] += n
+                else:
+                    out.append([a, n, v])
+            return np.array(out, dtype=np.int64).reshape(-1, 3)
+
+        return merge(runs_j), merge(runs_h)
+
     def _grad_csr(self, nvar):
         plan = self.plan
         vars_, gidx, grp = [], [], []
@@ -707,6 +738,9 @@ class DevicePlan:
             desc.persist[m] = lay.persist[m]
         desc.pdl = int(lay.pdl)
         desc.batchable = int(lay.specialised and not any(lay.persist))
+        self._fill = np.ascontiguousarray(np.concatenate([lay.fill_jac, lay.fill_hess]).reshape(-1), dtype=np.int64)
+        desc.host_fill = self._fill.ctypes.data_as(C.POINTER(C.c_int64))
+        desc.n_fill_jac, desc.n_fill_hess = len(lay.fill_jac), len(lay.fill_hess)
         n_obj, n_con = len(plan.obj_terms), len(plan.con_terms)
         bases = {
             _lib.MODE_SET: (n_con, 0), _lib.MODE_CONS: (0, 0), _lib.MODE_JAC: (0, 0),
