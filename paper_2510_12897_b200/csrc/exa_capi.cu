@@ -81,6 +81,9 @@ struct ExaWorkspace {
   cudaEvent_t fork = nullptr, join = nullptr;
   /* device staging for exa_eval_set_host (allocated on first use) */
   double *dx = nullptr, *dy = nullptr, *dc = nullptr, *dJ = nullptr, *dH = nullptr;
+  /* pinned host staging for pageable callers: x, mult | c, J ranges, H ranges */
+  double* hstage = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
 };
 
 struct ExaPlan {
@@ -355,6 +358,8 @@ void exa_workspace_destroy(ExaWorkspace* w) {
   cudaFree(w->dc);
   cudaFree(w->dJ);
   cudaFree(w->dH);
+  if (w->hstage) cudaFreeHost(w->hstage);
+  for (cudaEvent_t e : w->chunk_ev) cudaEventDestroy(e);
   if (w->fork) cudaEventDestroy(w->fork);
   if (w->join) cudaEventDestroy(w->join);
   if (w->aux) cudaStreamDestroy(w->aux);
@@ -638,7 +643,8 @@ int exa_eval_set_batch(ExaPlan* p, ExaWorkspace* ws, int64_t nsets, const double
 // ---------------------------------------------------------------------------
 namespace {
 struct FillPool {
-  struct Piece { double* dst; int64_t n; double v; };
+  // dst[0, n) = v, or (src) = src[0, n) once event ev (if any) has completed
+  struct Piece { double* dst; int64_t n; double v; const double* src = nullptr; cudaEvent_t ev = nullptr; };
   std::mutex call_mu;  // one fill at a time
   std::mutex mu;
   std::condition_variable cv;
@@ -649,7 +655,10 @@ struct FillPool {
   std::atomic<int> active{0};
 
   static void run(const Piece& q) {
-    if (q.v == 0.0 && !std::signbit(q.v)) {
+    if (q.src) {
+      if (q.ev) cudaEventSynchronize(q.ev);
+      std::memcpy(q.dst, q.src, q.n * sizeof(double));
+    } else if (q.v == 0.0 && !std::signbit(q.v)) {
       std::memset(q.dst, 0, q.n * sizeof(double));
     } else {
       for (int64_t i = 0; i < q.n; ++i) q.dst[i] = q.v;
@@ -713,15 +722,34 @@ FillPool& fill_pool() {
 }
 }  // namespace
 
-static void host_fill(const ExaPlan* p, double* jac, double* hess) {
-  constexpr int64_t kPiece = 32768;  // doubles (256 KB)
-  std::vector<FillPool::Piece> pcs;
+constexpr int64_t kPiece = 32768;  // doubles (256 KB) per host-pool piece
+
+static void add_fill(const ExaPlan* p, double* jac, double* hess, std::vector<FillPool::Piece>& pcs) {
   for (auto* rs : {&p->fill_jac, &p->fill_hess}) {
     double* out = rs == &p->fill_jac ? jac : hess;
     for (auto& r : *rs)
       for (int64_t o = 0; o < r.n; o += kPiece) pcs.push_back({out + r.a + o, r.n - o < kPiece ? r.n - o : kPiece, r.v});
   }
-  if (!pcs.empty()) fill_pool().fill(pcs);
+}
+
+static bool pageable(const void* ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+// D2H ranges (dst host, src device, doubles) of one host-path set
+struct Range { double* dst; const double* src; int64_t n; };
+
+static std::vector<Range> d2h_ranges(const ExaPlan* p, const ExaWorkspace* w, double* c, double* jac, double* hess) {
+  std::vector<Range> r;
+  if (p->ncon) r.push_back({c, w->dc, p->ncon});
+  for (auto& q : p->copy_jac) r.push_back({jac + q.first, w->dJ + q.first, q.second});
+  for (auto& q : p->copy_hess) r.push_back({hess + q.first, w->dH + q.first, q.second});
+  return r;
 }
 
 int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
@@ -737,32 +765,78 @@ int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const doubl
     CU(cudaMalloc((void**)&w->dJ, (p->n_jac > 0 ? p->n_jac : 1) * sizeof(double)));
     CU(cudaMalloc((void**)&w->dH, (p->n_hess > 0 ? p->n_hess : 1) * sizeof(double)));
   }
-  if (p->nvar) CU(cudaMemcpyAsync(w->dx, x, p->nvar * sizeof(double), cudaMemcpyHostToDevice, st));
-  if (p->ncon) CU(cudaMemcpyAsync(w->dy, mult, p->ncon * sizeof(double), cudaMemcpyHostToDevice, st));
+  const bool pg_in = (p->nvar && pageable(x)) || (p->ncon && pageable(mult));
+  const bool pg_out = (p->ncon && pageable(c)) || (p->n_jac && pageable(jac)) || (p->n_hess && pageable(hess));
+  if ((pg_in || pg_out) && !w->hstage) {  // pinned staging for pageable callers (numpy arrays)
+    CU(cudaHostAlloc((void**)&w->hstage, (p->nvar + 2 * p->ncon + p->n_jac + p->n_hess + 1) * sizeof(double),
+                     cudaHostAllocDefault));
+  }
+  const double* xs = x;
+  const double* ys = mult;
+  if (pg_in) {  // pageable inputs: host threads copy them into pinned staging, then one DMA each
+    std::vector<FillPool::Piece> pcs;
+    for (int64_t o = 0; o < p->nvar; o += kPiece)
+      pcs.push_back({w->hstage + o, p->nvar - o < kPiece ? p->nvar - o : kPiece, 0.0, x + o});
+    for (int64_t o = 0; o < p->ncon; o += kPiece)
+      pcs.push_back({w->hstage + p->nvar + o, p->ncon - o < kPiece ? p->ncon - o : kPiece, 0.0, mult + o});
+    CU(cudaStreamSynchronize(st));  // the staging may still feed an earlier set's H2D
+    fill_pool().fill(pcs);
+    xs = w->hstage;
+    ys = w->hstage + p->nvar;
+  }
+  if (p->nvar) CU(cudaMemcpyAsync(w->dx, xs, p->nvar * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (p->ncon) CU(cudaMemcpyAsync(w->dy, ys, p->ncon * sizeof(double), cudaMemcpyHostToDevice, st));
   if (int rc = exa_eval_set(p, w, w->dx, w->dy, w_obj, w->dc, w->dJ, w->dH, stream)) return rc;
-  // D2H of everything but the constant runs (one batched call on a real
-  // stream), then the constant runs written on the host while the DMA runs
-  std::vector<void*> dst, src;
-  std::vector<size_t> len;
-  if (p->ncon) { dst.push_back(c); src.push_back(w->dc); len.push_back(p->ncon * sizeof(double)); }
-  for (auto& r : p->copy_jac) {
-    dst.push_back(jac + r.first); src.push_back(w->dJ + r.first); len.push_back(r.second * sizeof(double));
-  }
-  for (auto& r : p->copy_hess) {
-    dst.push_back(hess + r.first); src.push_back(w->dH + r.first); len.push_back(r.second * sizeof(double));
-  }
-  if (!dst.empty()) {
-    if (st != nullptr && st != cudaStreamLegacy && st != cudaStreamPerThread) {
-      cudaMemcpyAttributes at = {};
-      at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-      size_t ai = 0, fidx = 0;
-      CU(cudaMemcpyBatchAsync(dst.data(), src.data(), len.data(), dst.size(), &at, &ai, 1, &fidx, st));
-    } else {
-      for (size_t i = 0; i < dst.size(); ++i) CU(cudaMemcpyAsync(dst[i], src[i], len[i], cudaMemcpyDeviceToHost, st));
+  std::vector<FillPool::Piece> pcs;
+  if (pg_out) {
+    // pageable outputs: DMA each range, in 2 MB chunks, into pinned staging
+    // (event per chunk); host threads copy chunk k into the caller's arrays
+    // while later chunks are still in flight.  Returns with outputs complete.
+    constexpr int64_t kChunk = 262144;  // doubles
+    double* hs = w->hstage + p->nvar + p->ncon;
+    int64_t at = 0;
+    size_t ne = 0;
+    for (const Range& r : d2h_ranges(p, w, c, jac, hess)) {
+      for (int64_t o = 0; o < r.n; o += kChunk) {
+        const int64_t n = r.n - o < kChunk ? r.n - o : kChunk;
+        CU(cudaMemcpyAsync(hs + at, r.src + o, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (ne == w->chunk_ev.size()) {
+          cudaEvent_t e;
+          CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          w->chunk_ev.push_back(e);
+        }
+        cudaEvent_t e = w->chunk_ev[ne++];
+        CU(cudaEventRecord(e, st));
+        for (int64_t q = 0; q < n; q += kPiece)
+          pcs.push_back({r.dst + o + q, n - q < kPiece ? n - q : kPiece, 0.0, hs + at + q, e});
+        at += n;
+      }
+    }
+  } else {
+    // pinned outputs: D2H of everything but the constant runs (one batched
+    // call on a real stream); the constant runs are written meanwhile
+    std::vector<void*> dst, src;
+    std::vector<size_t> len;
+    for (const Range& r : d2h_ranges(p, w, c, jac, hess)) {
+      dst.push_back(r.dst);
+      src.push_back((void*)r.src);
+      len.push_back(r.n * sizeof(double));
+    }
+    if (!dst.empty()) {
+      if (st != nullptr && st != cudaStreamLegacy && st != cudaStreamPerThread) {
+        cudaMemcpyAttributes at = {};
+        at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+        size_t ai = 0, fidx = 0;
+        CU(cudaMemcpyBatchAsync(dst.data(), src.data(), len.data(), dst.size(), &at, &ai, 1, &fidx, st));
+      } else {
+        for (size_t i = 0; i < dst.size(); ++i)
+          CU(cudaMemcpyAsync(dst[i], src[i], len[i], cudaMemcpyDeviceToHost, st));
+      }
     }
   }
-  host_fill(p, jac, hess);
+  add_fill(p, jac, hess, pcs);
+  if (!pcs.empty()) fill_pool().fill(pcs);
   return 0;
 }
 

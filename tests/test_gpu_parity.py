@@ -260,6 +260,10 @@ def test_host_buffer_c_abi_matches_oracle(name):
         torch.cuda.synchronize()
         lib.exa_workspace_destroy(wsp)
         outs.append((hc.numpy().copy(), hJ.numpy().copy(), hH.numpy().copy()))
+    # the drop-in numpy call (pageable arrays: pinned staging, chunked D2H)
+    npo = [np.full(n, np.nan) for n in (model.ncon, model.plan.n_jac_slots, model.plan.n_hess_slots)]
+    eval_callback_set(model, np.array(x), np.array(y), w, *npo)
+    outs.append(tuple(npo))
     for c, J, H in outs:
         for a, d in zip((c, J, H), dev):
             assert np.array_equal(a.view(np.int64), d.view(np.int64))
