@@ -172,6 +172,16 @@ int exa_eval_set_batch(ExaPlan* plan, ExaWorkspace* ws, int64_t nsets, const dou
 int exa_eval_set_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, const double* mult_host,
                       double obj_weight, double* c_host, double* jac_host, double* hess_host,
                       exa_stream_t stream);
+/* The separate callbacks with HOST buffers (the reference IPM calls
+ * eval_constraints / eval_jacobian / eval_hessian with numpy arrays every
+ * iteration; autodiff.py:566,588,615): same staging, copies and constant-run
+ * fill as exa_eval_set_host.  Pageable (unregistered) host buffers go through
+ * the workspace's pinned staging and the call returns with the outputs
+ * complete; pinned buffers are filled asynchronously on `stream`. */
+int exa_eval_cons_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, double* c_host, exa_stream_t stream);
+int exa_eval_jac_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, double* jac_host, exa_stream_t stream);
+int exa_eval_hess_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, const double* mult_host,
+                       double obj_weight, double* hess_host, exa_stream_t stream);
 /* out[k] = 0 + sum_{e in [ptr[k], ptr[k+1])} raw[ent[e]], sequentially in e
  * order (np.bincount order); with ent sorted by raw slot within each k this is
  * CompressedPattern.sum_values.  All pointers are device pointers. */

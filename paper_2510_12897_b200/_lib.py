@@ -71,6 +71,9 @@ SIGNATURES = {
     "exa_eval_hess": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp]),
     "exa_eval_set": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp, vp, vp]),
     "exa_eval_set_host": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp, vp, vp]),
+    "exa_eval_cons_host": (C.c_int, [vp, vp, vp, vp, vp]),
+    "exa_eval_jac_host": (C.c_int, [vp, vp, vp, vp, vp]),
+    "exa_eval_hess_host": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp]),
     "exa_eval_set_batch": (C.c_int, [vp, vp, i64, vp, vp, dbl, vp, vp, vp, vp]),
     "exa_segment_sum": (C.c_int, [i64, vp, vp, vp, vp, vp]),
     "exa_kkt_values": (C.c_int, [i64, vp, vp, vp, vp, dbl, dbl, vp, vp]),

@@ -157,6 +157,33 @@ def eval_objective(model, x) -> float:
     return float(out.item())
 
 
+def _host_outputs(*outs) -> bool:
+    """Outputs the C ABI host path can write directly: contiguous, writable
+    float64 numpy arrays."""
+    return all(isinstance(b, np.ndarray) and b.dtype == np.float64 and b.flags.c_contiguous and b.flags.writeable
+               for b in outs)
+
+
+def _host_call(dp, name: str, callback: str, *args) -> None:
+    """numpy in/out through ``exa_eval_*_host`` (H2D, kernel, D2H of the
+    x-dependent ranges, constant runs filled on the host); numpy args become
+    pointers (inputs made contiguous), floats pass through."""
+    torch = _torch()
+    stream = torch.cuda.current_stream(torch.device("cuda", dp.device))
+    keep, conv = [], []
+    for a in args:
+        if isinstance(a, np.ndarray):
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            keep.append(a)
+            conv.append(a.ctypes.data if a.size else 0)
+        else:
+            conv.append(a)
+    s = C.c_void_p(stream.cuda_stream)
+    _lib.check(getattr(dp._lib, name)(dp.handle, None, *conv, s), name)
+    _raise_domain(dp, s, callback)
+    stream.synchronize()
+
+
 def eval_gradient(model, x, out_g) -> None:
     x = _check_x(model, x)
     if _shape(out_g) != (model.nvar,):
@@ -177,6 +204,8 @@ def eval_constraints(model, x, out_c) -> None:
     if _shape(out_c) != (model.ncon,):
         raise ValueError(f"constraint buffer has shape {_shape(out_c)}, expected ({model.ncon},)")
     dp = _dplan(model)
+    if not _is_cuda(x) and _host_outputs(out_c):
+        return _host_call(dp, "exa_eval_cons_host", "cons", x, out_c)
     st = _Stage(dp)
     xp, cp = st.inp(x), st.out(out_c, model.ncon)
     s = st.stream()
@@ -196,6 +225,8 @@ def eval_jacobian(model, x, out_vals) -> None:
     if _shape(out_vals) != (n,):
         raise ValueError(f"jacobian buffer has shape {_shape(out_vals)}, expected ({n},)")
     dp = _dplan(model)
+    if not _is_cuda(x) and _host_outputs(out_vals):
+        return _host_call(dp, "exa_eval_jac_host", "jac", x, out_vals)
     st = _Stage(dp)
     xp, jp = st.inp(x), st.out(out_vals, n)
     s = st.stream()
@@ -228,6 +259,8 @@ def eval_hessian(model, x, mult, obj_weight: float, out_vals) -> None:
     if _shape(out_vals) != (n,):
         raise ValueError(f"hessian buffer has shape {_shape(out_vals)}, expected ({n},)")
     dp = _dplan(model)
+    if not _is_cuda(x) and not _is_cuda(mult) and _host_outputs(out_vals):
+        return _host_call(dp, "exa_eval_hess_host", "hess", x, mult, float(obj_weight), out_vals)
     st = _Stage(dp)
     xp = st.inp(x)
     yp = st.inp(mult) if model.ncon else 0
@@ -252,20 +285,8 @@ def eval_callback_set(model, x, mult, obj_weight: float, out_c, out_jac, out_hes
         if _shape(buf) != (n,):
             raise ValueError(f"{what} buffer has shape {_shape(buf)}, expected ({n},)")
     dp = _dplan(model)
-    bufs = (x, mult, out_c, out_jac, out_hess)
-    if all(isinstance(b, np.ndarray) and b.dtype == np.float64 and b.flags.c_contiguous for b in bufs) \
-            and all(b.flags.writeable for b in bufs[2:]):
-        # all-numpy call: the C ABI host path (H2D, set kernel, D2H of the
-        # x-dependent ranges straight into the caller's arrays, constant runs
-        # filled on the host)
-        torch = _torch()
-        s = C.c_void_p(torch.cuda.current_stream(torch.device("cuda", dp.device)).cuda_stream)
-        ptr = [b.ctypes.data if b.size else 0 for b in bufs]
-        _lib.check(dp._lib.exa_eval_set_host(dp.handle, None, ptr[0], ptr[1], float(obj_weight), ptr[2], ptr[3],
-                                             ptr[4], s), "eval_set_host")
-        _raise_domain(dp, s, "set")
-        torch.cuda.current_stream(torch.device("cuda", dp.device)).synchronize()
-        return
+    if not _is_cuda(x) and not _is_cuda(mult) and _host_outputs(out_c, out_jac, out_hess):
+        return _host_call(dp, "exa_eval_set_host", "set", x, mult, float(obj_weight), out_c, out_jac, out_hess)
     st = _Stage(dp)
     xp = st.inp(x)
     yp = st.inp(mult) if model.ncon else 0

@@ -727,6 +727,7 @@ constexpr int64_t kPiece = 32768;  // doubles (256 KB) per host-pool piece
 static void add_fill(const ExaPlan* p, double* jac, double* hess, std::vector<FillPool::Piece>& pcs) {
   for (auto* rs : {&p->fill_jac, &p->fill_hess}) {
     double* out = rs == &p->fill_jac ? jac : hess;
+    if (!out) continue;
     for (auto& r : *rs)
       for (int64_t o = 0; o < r.n; o += kPiece) pcs.push_back({out + r.a + o, r.n - o < kPiece ? r.n - o : kPiece, r.v});
   }
@@ -746,17 +747,22 @@ struct Range { double* dst; const double* src; int64_t n; };
 
 static std::vector<Range> d2h_ranges(const ExaPlan* p, const ExaWorkspace* w, double* c, double* jac, double* hess) {
   std::vector<Range> r;
-  if (p->ncon) r.push_back({c, w->dc, p->ncon});
-  for (auto& q : p->copy_jac) r.push_back({jac + q.first, w->dJ + q.first, q.second});
-  for (auto& q : p->copy_hess) r.push_back({hess + q.first, w->dH + q.first, q.second});
+  if (c && p->ncon) r.push_back({c, w->dc, p->ncon});
+  if (jac)
+    for (auto& q : p->copy_jac) r.push_back({jac + q.first, w->dJ + q.first, q.second});
+  if (hess)
+    for (auto& q : p->copy_hess) r.push_back({hess + q.first, w->dH + q.first, q.second});
   return r;
 }
 
-int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
-                      double* jac, double* hess, exa_stream_t stream) {
+// Host-buffer form of one callback (mode SET, CONS, JAC or HESS): H2D of the
+// inputs the mode reads, the device callback on the workspace's staging, D2H
+// of its x-dependent output ranges, constant runs filled on the host.  Null
+// output pointers are the outputs the mode does not produce.
+static int host_eval(ExaPlan* p, ExaWorkspace* ws, int mode, const double* x, const double* mult, double w_obj,
+                     double* c, double* jac, double* hess, cudaStream_t st) {
   if (!p) return fail("null plan");
   ExaWorkspace* w = ws ? ws : p->dflt;
-  cudaStream_t st = (cudaStream_t)stream;
   if (!w->dx) {  // first use: device staging sized for this plan
     CU(cudaSetDevice(p->device));
     CU(cudaMalloc((void**)&w->dx, (p->nvar > 0 ? p->nvar : 1) * sizeof(double)));
@@ -765,8 +771,13 @@ int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const doubl
     CU(cudaMalloc((void**)&w->dJ, (p->n_jac > 0 ? p->n_jac : 1) * sizeof(double)));
     CU(cudaMalloc((void**)&w->dH, (p->n_hess > 0 ? p->n_hess : 1) * sizeof(double)));
   }
-  const bool pg_in = (p->nvar && pageable(x)) || (p->ncon && pageable(mult));
-  const bool pg_out = (p->ncon && pageable(c)) || (p->n_jac && pageable(jac)) || (p->n_hess && pageable(hess));
+  if (mode != EXA_MODE_SET && mode != EXA_MODE_HESS) mult = nullptr;
+  if (mode != EXA_MODE_SET && mode != EXA_MODE_CONS) c = nullptr;
+  if (mode != EXA_MODE_SET && mode != EXA_MODE_JAC) jac = nullptr;
+  if (mode != EXA_MODE_SET && mode != EXA_MODE_HESS) hess = nullptr;
+  const bool pg_in = (p->nvar && pageable(x)) || (mult && p->ncon && pageable(mult));
+  const bool pg_out = (c && p->ncon && pageable(c)) || (jac && p->n_jac && pageable(jac)) ||
+                      (hess && p->n_hess && pageable(hess));
   if ((pg_in || pg_out) && !w->hstage) {  // pinned staging for pageable callers (numpy arrays)
     CU(cudaHostAlloc((void**)&w->hstage, (p->nvar + 2 * p->ncon + p->n_jac + p->n_hess + 1) * sizeof(double),
                      cudaHostAllocDefault));
@@ -777,7 +788,7 @@ int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const doubl
     std::vector<FillPool::Piece> pcs;
     for (int64_t o = 0; o < p->nvar; o += kPiece)
       pcs.push_back({w->hstage + o, p->nvar - o < kPiece ? p->nvar - o : kPiece, 0.0, x + o});
-    for (int64_t o = 0; o < p->ncon; o += kPiece)
+    for (int64_t o = 0; mult && o < p->ncon; o += kPiece)
       pcs.push_back({w->hstage + p->nvar + o, p->ncon - o < kPiece ? p->ncon - o : kPiece, 0.0, mult + o});
     CU(cudaStreamSynchronize(st));  // the staging may still feed an earlier set's H2D
     fill_pool().fill(pcs);
@@ -785,8 +796,16 @@ int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const doubl
     ys = w->hstage + p->nvar;
   }
   if (p->nvar) CU(cudaMemcpyAsync(w->dx, xs, p->nvar * sizeof(double), cudaMemcpyHostToDevice, st));
-  if (p->ncon) CU(cudaMemcpyAsync(w->dy, ys, p->ncon * sizeof(double), cudaMemcpyHostToDevice, st));
-  if (int rc = exa_eval_set(p, w, w->dx, w->dy, w_obj, w->dc, w->dJ, w->dH, stream)) return rc;
+  if (mult && p->ncon) CU(cudaMemcpyAsync(w->dy, ys, p->ncon * sizeof(double), cudaMemcpyHostToDevice, st));
+  int rc = 0;
+  switch (mode) {
+    case EXA_MODE_SET: rc = exa_eval_set(p, w, w->dx, w->dy, w_obj, w->dc, w->dJ, w->dH, st); break;
+    case EXA_MODE_CONS: rc = exa_eval_cons(p, w, w->dx, w->dc, st); break;
+    case EXA_MODE_JAC: rc = exa_eval_jac(p, w, w->dx, w->dJ, st); break;
+    case EXA_MODE_HESS: rc = exa_eval_hess(p, w, w->dx, w->dy, w_obj, w->dH, st); break;
+    default: return fail("host_eval: mode %d has no host form", mode);
+  }
+  if (rc) return rc;
   std::vector<FillPool::Piece> pcs;
   if (pg_out) {
     // pageable outputs: DMA each range, in 2 MB chunks, into pinned staging
@@ -838,6 +857,24 @@ int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const doubl
   add_fill(p, jac, hess, pcs);
   if (!pcs.empty()) fill_pool().fill(pcs);
   return 0;
+}
+
+int exa_eval_set_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
+                      double* jac, double* hess, exa_stream_t stream) {
+  return host_eval(p, ws, EXA_MODE_SET, x, mult, w_obj, c, jac, hess, (cudaStream_t)stream);
+}
+
+int exa_eval_cons_host(ExaPlan* p, ExaWorkspace* ws, const double* x, double* c, exa_stream_t stream) {
+  return host_eval(p, ws, EXA_MODE_CONS, x, nullptr, 0.0, c, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+int exa_eval_jac_host(ExaPlan* p, ExaWorkspace* ws, const double* x, double* jac, exa_stream_t stream) {
+  return host_eval(p, ws, EXA_MODE_JAC, x, nullptr, 0.0, nullptr, jac, nullptr, (cudaStream_t)stream);
+}
+
+int exa_eval_hess_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj,
+                       double* hess, exa_stream_t stream) {
+  return host_eval(p, ws, EXA_MODE_HESS, x, mult, w_obj, nullptr, nullptr, hess, (cudaStream_t)stream);
 }
 
 int exa_eval_cons(ExaPlan* p, ExaWorkspace* ws, const double* x, double* c, exa_stream_t stream) {

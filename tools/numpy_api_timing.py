@@ -1,0 +1,13 @@
+"""Per-call time of the drop-in numpy callbacks (pageable host arrays) at case13659."""
+import time, numpy as np, torch
+from paper_2510_12897_b200 import workloads, eval_constraints, eval_jacobian, eval_hessian, eval_callback_set
+r = workloads.build_workload("case13659")
+m = r[0] if isinstance(r, tuple) else r
+x, y, w = workloads.eval_inputs(m, 0)[:3]
+c, J, H = np.empty(m.ncon), np.empty(m.plan.n_jac_slots), np.empty(m.plan.n_hess_slots)
+for name, f in (("cons", lambda: eval_constraints(m, x, c)), ("jac", lambda: eval_jacobian(m, x, J)),
+                ("hess", lambda: eval_hessian(m, x, y, 1.0, H)), ("set", lambda: eval_callback_set(m, x, y, 1.0, c, J, H))):
+    f(); f()
+    t0 = time.perf_counter(); n = 50
+    for _ in range(n): f()
+    print(name, f"{(time.perf_counter() - t0) / n * 1e6:.0f} us/call (numpy)")
