@@ -493,6 +493,7 @@ def main():
                          f"one set per step, {NS} streams in round robin; constant J/H runs "
                          f"({filled / 1e6:.1f} MB) written by host threads, not copied"),
                 "host_filled_bytes_per_step": filled,
+                "d2h_GBps": d2h * e2e_value / (1 if sharded else ws) / 1e9,
                 "sequential_value": e2e_seq, "numpy_api_value": e2e_numpy},
         "clocks": sampler.summary(),
         "batched": batched,
