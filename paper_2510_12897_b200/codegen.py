@@ -817,13 +817,16 @@ def group_source(gid: int, entries: list, augs: list = ()) -> str:
     out.extend(early)
     if xkey:
         out.append("  EXA_TP(1, " + " + ".join(f"xg{n}" for n in range(len(xkey))) + ");")
+    out.append("  EXA_GRID_RELEASE_MID(1);")
     # phase stamp 2 after the first sin/cos
     lines = list(g.lines)
     for i, ln in enumerate(lines):
         m_ = re.search(r"exa_sincos\(.*?&(\w+), &(\w+)\)", ln)
         if m_:
             lines.insert(i + 1, f"  EXA_TP(2, {m_.group(1)} + {m_.group(2)});")
+            lines.insert(i + 2, "  EXA_GRID_RELEASE_MID(2);")
             break
+
     out.extend(lines)
     out.append("}")
     return "\n".join(out)

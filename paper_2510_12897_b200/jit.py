@@ -63,6 +63,7 @@ PREFETCH_CHUNK = int(os.environ.get("EXA_PREFETCH_CHUNK", "32768"))
 # library sets the launch attribute only for modules built with the waits.
 PDL = os.environ.get("EXA_PDL", "1") == "1"
 PDL_EARLY = os.environ.get("EXA_PDL_EARLY", "0") == "1"
+PDL_MID = int(os.environ.get("EXA_PDL_MID", "2"))  # release point inside term groups (see EXA_GRID_RELEASE_MID)
 
 _lock = threading.Lock()
 _mem_cache: dict = {}
@@ -112,6 +113,17 @@ __device__ __forceinline__ void exa_report(const ExaArgs& A, int rank, int instr
 #else
 #define EXA_GRID_WAIT() do {} while (0)
 #define EXA_GRID_RELEASE() do {} while (0)
+#endif
+// release the dependent grid from inside the heavy segments: 2 (default) =
+// once a term group's sin/cos are done (the rest is Hessian arithmetic and
+// stores; the next grid's CTAs take slots as this grid's CTAs exit and load
+// their plan data during this grid's store tail: case13659 7.01 -> 6.91 us);
+// 1 = once the gathers are issued (7.06; also releasing row buckets after
+// their gathers: 7.06); 0 = only at CTA end (7.01)
+#if EXA_PDL && EXA_PDL_MID
+#define EXA_GRID_RELEASE_MID(k) do { if ((k) == EXA_PDL_MID) asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); } while (0)
+#else
+#define EXA_GRID_RELEASE_MID(k) do {} while (0)
 #endif
 // diagnostics (EXA_TRACE=1 builds only): per warp and virtual CTA, 12 words
 // (SM id, virtual CTA, clock64 start/end, globaltimer start/end, 4 phase
@@ -598,6 +610,7 @@ def module_source(patterns, layout=None, threads: int = 32) -> str:
     parts = ["// generated by paper_2510_12897_b200.jit",
              f"#define EXA_PDL {1 if PDL else 0}",
              f"#define EXA_PDL_EARLY {1 if PDL_EARLY else 0}",
+             f"#define EXA_PDL_MID {PDL_MID}",
              f"#define EXA_TRACE {1 if TRACE else 0}",
              "#define EXA_SC_CONST 1" if SC_TABLE == "const" else "",
              f"#define EXA_TRACE_NT {max(threads, THREADS_HEAVY) * max(1, PERSIST)}",
