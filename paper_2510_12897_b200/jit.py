@@ -63,7 +63,7 @@ PREFETCH_CHUNK = int(os.environ.get("EXA_PREFETCH_CHUNK", "32768"))
 # library sets the launch attribute only for modules built with the waits.
 PDL = os.environ.get("EXA_PDL", "1") == "1"
 PDL_EARLY = os.environ.get("EXA_PDL_EARLY", "0") == "1"
-PDL_MID = int(os.environ.get("EXA_PDL_MID", "2"))  # release point inside term groups (see EXA_GRID_RELEASE_MID)
+PDL_MID = int(os.environ.get("EXA_PDL_MID", "1"))  # release point inside term groups (see EXA_GRID_RELEASE_MID)
 
 _lock = threading.Lock()
 _mem_cache: dict = {}
@@ -114,12 +114,12 @@ __device__ __forceinline__ void exa_report(const ExaArgs& A, int rank, int instr
 #define EXA_GRID_WAIT() do {} while (0)
 #define EXA_GRID_RELEASE() do {} while (0)
 #endif
-// release the dependent grid from inside the heavy segments: 2 (default) =
-// once a term group's sin/cos are done (the rest is Hessian arithmetic and
-// stores; the next grid's CTAs take slots as this grid's CTAs exit and load
-// their plan data during this grid's store tail: case13659 7.01 -> 6.91 us);
-// 1 = once the gathers are issued (7.06; also releasing row buckets after
-// their gathers: 7.06); 0 = only at CTA end (7.01)
+// release the dependent grid from inside the term groups: 1 (default) = once
+// a group's gathers are issued, 2 = once its sin/cos are done, 0 = only at
+// CTA end (row buckets and terms always release at CTA end).  The next grid's
+// CTAs take slots as this grid's CTAs exit and load their plan data during
+// this grid's store tail.  case13659 (buckets dispatched first) 6.94 / 6.70 /
+// 6.53 us for 0 / 2 / 1; MP96 41.44 (2) -> 41.26 (1)
 #if EXA_PDL && EXA_PDL_MID
 #define EXA_GRID_RELEASE_MID(k) do { if ((k) == EXA_PDL_MID) asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); } while (0)
 #else
