@@ -63,6 +63,16 @@ PREFETCH_CHUNK = int(os.environ.get("EXA_PREFETCH_CHUNK", "32768"))
 # library sets the launch attribute only for modules built with the waits.
 PDL = os.environ.get("EXA_PDL", "1") == "1"
 PDL_EARLY = os.environ.get("EXA_PDL_EARLY", "0") == "1"
+# row buckets' release point: 1 = once their entry gathers are issued, 2 = right
+# after the wait, 0 = CTA end; "auto" = 1 for one-wave sets (case13659 6.53 ->
+# 6.40 us), 0 for many-wave ones (MP96: 1 costs 2%, N-1 1%)
+PDL_MID_BKT = os.environ.get("EXA_PDL_MID_BKT", "auto")
+
+
+def _bkt_release(threads: int) -> int:
+    if PDL_MID_BKT == "auto":
+        return 1 if threads == 32 else 0
+    return int(PDL_MID_BKT)
 PDL_MID = int(os.environ.get("EXA_PDL_MID", "1"))  # release point inside term groups (see EXA_GRID_RELEASE_MID)
 
 _lock = threading.Lock()
@@ -404,6 +414,8 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, m):
           f"    const int2 er = __ldg(reinterpret_cast<const int2*>(A.i32 + {bk['pair_off']}LL) + 32 * q + lane);",
           "    const int e = er.x, rc = er.y;",
           "    EXA_GRID_WAIT();"]
+    if _bkt_release(threads):  # warp rows: release right after the wait
+        L.append("    EXA_GRID_RELEASE();")
     L.append("    const double wrow = " + ("__ldg(A.y + T.row_offset + r);" if want_h else "0.0;"))
     L += ["    double v = 0.0;",
           "    if (lane == 0) {"]
@@ -484,6 +496,8 @@ def _kernel_source(layout, m, half, kname) -> str:
                 if c0 == 0:
                     b_.append(f"    EXA_TP(0, {'e0' if dd else 'r'});")
                     b_.append("    EXA_GRID_WAIT();")
+                    if _bkt_release(threads) == 2:
+                        b_.append("    EXA_GRID_RELEASE();")
                     b_.append("    const double wrow = " + ("__ldg(A.y + T.row_offset + r);" if want_h else "0.0;"))
                     if want_v:
                         # base value first: its gathers issue with the entries' (a later
@@ -498,6 +512,8 @@ def _kernel_source(layout, m, half, kname) -> str:
                 if c0 == 0:
                     if ks and need_x:
                         b_.append("    EXA_TP(1, " + " + ".join(f"xv{k}" for k in ks) + ");")
+                        if _bkt_release(threads) == 1:
+                            b_.append("    EXA_GRID_RELEASE();")
                     # base term J/H after the entry gathers are issued (in-order issue:
                     # its stores wait on its own gather and would hold the others back)
                     if base_mode and info["base_k"]:
