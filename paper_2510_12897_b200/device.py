@@ -425,13 +425,16 @@ class HostLayout:
         if order is None and choose_threads(sum(sg[2] for sg in segs[_lib.MODE_SET])) == 32:
             order = "BOG"
         if order:
-            def prio(sg):  # order = permutation of "BGO": buckets, groups, other terms
+            flags = order[3:]
+
+            def prio(sg):  # order[:3] = permutation of "BGO": buckets, groups, other terms
                 t, kind, _ = sg
                 if (kind & 15) == SEG_BUCKET:
-                    return order.index("B")
+                    d = self.buckets[t]["buckets"][kind >> 4]["d"]
+                    return (order.index("B"), -d if "d" in flags else 0, -t if "t" in flags else 0)
                 if t in self.group_of:
-                    return order.index("G")
-                return order.index("O")
+                    return (order.index("G"), -t if "r" in flags else 0, 0)
+                return (order.index("O"), 0, 0)
             for m in segs:
                 segs[m] = sorted(segs[m], key=prio)
         # experiment knob: keep only heavy (k > 2) or only light segments
