@@ -438,6 +438,18 @@ def main():
     for _ in range(n_np):
         eval_callback_set(model, xn, yn, 1.0, cn, Jn, Hn)
     e2e_numpy = n_np / (time.perf_counter() - t0)
+    # ... with the outputs in page-locked arrays (paper_2510_12897_b200.empty_pinned)
+    from paper_2510_12897_b200 import empty_pinned
+
+    cp_, Jp_, Hp_ = (empty_pinned(n) for n in (model.ncon, model.plan.n_jac_slots, model.plan.n_hess_slots))
+    xp_, yp_ = empty_pinned(model.nvar), empty_pinned(model.ncon)
+    xp_[:], yp_[:] = xn, yn
+    eval_callback_set(model, xp_, yp_, 1.0, cp_, Jp_, Hp_)
+    t0 = time.perf_counter()
+    for _ in range(n_np):
+        eval_callback_set(model, xp_, yp_, 1.0, cp_, Jp_, Hp_)
+    e2e_numpy_pinned = n_np / (time.perf_counter() - t0)
+    assert np.array_equal(Hp_, Hn) and np.array_equal(Jp_, Jn)
     # latency view: one set at a time, synchronised per set
     t0 = time.perf_counter()
     for i in range(n_e2e // NS):
@@ -494,7 +506,8 @@ def main():
                          f"({filled / 1e6:.1f} MB) written by host threads, not copied"),
                 "host_filled_bytes_per_step": filled,
                 "d2h_GBps": d2h * e2e_value / (1 if sharded else ws) / 1e9,
-                "sequential_value": e2e_seq, "numpy_api_value": e2e_numpy},
+                "sequential_value": e2e_seq, "numpy_api_value": e2e_numpy,
+                "numpy_api_pinned_value": e2e_numpy_pinned},
         "clocks": sampler.summary(),
         "batched": batched,
         "gpu_launches": args.steps * S,

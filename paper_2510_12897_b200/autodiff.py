@@ -157,6 +157,16 @@ def eval_objective(model, x) -> float:
     return float(out.item())
 
 
+def empty_pinned(n: int) -> np.ndarray:
+    """An uninitialised float64 numpy array of length ``n`` in page-locked
+    host memory.  Callback inputs and outputs allocated this way skip the
+    pageable staging of the host path (case13659 set through the numpy API:
+    476 -> 367 us per call; pageable outputs alone cost nothing extra, their
+    chunked staging overlaps the DMA, pageable inputs cost ~110 us)."""
+    torch = _torch()
+    return torch.empty(int(n), dtype=torch.float64).pin_memory().numpy()
+
+
 def _host_outputs(*outs) -> bool:
     """Outputs the C ABI host path can write directly: contiguous, writable
     float64 numpy arrays."""

@@ -11,3 +11,16 @@ for name, f in (("cons", lambda: eval_constraints(m, x, c)), ("jac", lambda: eva
     t0 = time.perf_counter(); n = 50
     for _ in range(n): f()
     print(name, f"{(time.perf_counter() - t0) / n * 1e6:.0f} us/call (numpy)")
+
+# page-locked arrays (paper_2510_12897_b200.empty_pinned): outputs only, then inputs too
+from paper_2510_12897_b200 import empty_pinned
+
+cp_, Jp_, Hp_ = (empty_pinned(n) for n in (m.ncon, m.plan.n_jac_slots, m.plan.n_hess_slots))
+xp_, yp_ = empty_pinned(m.nvar), empty_pinned(m.ncon)
+xp_[:], yp_[:] = x, y
+for name, f in (("set, pinned outputs", lambda: eval_callback_set(m, x, y, 1.0, cp_, Jp_, Hp_)),
+                ("set, pinned in+out", lambda: eval_callback_set(m, xp_, yp_, 1.0, cp_, Jp_, Hp_))):
+    f(); f()
+    t0 = time.perf_counter(); n = 50
+    for _ in range(n): f()
+    print(name, f"{(time.perf_counter() - t0) / n * 1e6:.0f} us/call")
