@@ -52,6 +52,7 @@ GROUP_MAX = int(os.environ.get("EXA_GROUP_MAX", "2"))
 ATTACH = os.environ.get("EXA_ATTACH", "1") == "1"  # light terms join heavy groups
 GROUP_RPT = int(os.environ.get("EXA_GROUP_RPT", "1"))  # records per thread of term groups (ILP)
 ATTACH_AUGS = os.environ.get("EXA_ATTACH_AUGS", "1") == "1"  # groups write aligned augments' J/H
+HALF_ROWS = os.environ.get("EXA_HALF_ROWS", "1") == "1"  # long bucket rows of <= 15 entries: half a warp each
 
 # Models with at most this many terms get a *specialised* module (metadata
 # compiled in as constants); larger ones (e.g. thousands of per-instance
@@ -215,8 +216,9 @@ def _bucket_layout(base_tp, augs, nvar):
     records (the row thread also writes their Jacobian/Hessian slots in the
     fused set kernel), -1 past a row's d; or None when the block does not fit
     the encoding.  Rows with more than BUCKET_WMAX contributions form the
-    class W = 32 (listed first): one warp per row, arrays (n, 32) row-major,
-    lane 0 reserved for the base term."""
+    classes W = 32 and 16 (listed first): one warp (half warp, for rows of at
+    most 15 contributions) per row, arrays (n, W) row-major, lane 0 reserved
+    for the base term."""
     if len(augs) > (1 << BUCKET_SEL_BITS) or nvar >= (1 << BUCKET_GID_BITS):
         return None
     n = base_tp.nrec
@@ -244,15 +246,21 @@ def _bucket_layout(base_tp, augs, nvar):
     # (class W = 32, entries laid out row-major so each warp reads 128 B)
     long_ = width > BUCKET_WMAX
     if long_.any():
-        rows = np.flatnonzero(long_)
-        ent = np.full((rows.size, 32), -1, dtype=np.int64)
-        rec = np.full((rows.size, 32), -1, dtype=np.int64)
-        for q, rr in enumerate(rows.tolist()):
-            dd = int(counts[rr])
-            ent[q, 1:dd + 1] = ents[ptr[rr]:ptr[rr] + dd]
-            rec[q, 1:dd + 1] = recs[ptr[rr]:ptr[rr] + dd]
+        lrows_ = np.flatnonzero(long_)
+        # rows with <= 15 contributions take half a warp (two rows per warp)
+        split = [(32, lrows_[counts[lrows_] > 15]), (16, lrows_[counts[lrows_] <= 15])] if HALF_ROWS \
+            else [(32, lrows_)]
+        for LW, rows in split:
+            if rows.size == 0:
+                continue
+            ent = np.full((rows.size, LW), -1, dtype=np.int64)
+            rec = np.full((rows.size, LW), -1, dtype=np.int64)
+            for q, rr in enumerate(rows.tolist()):
+                dd = int(counts[rr])
+                ent[q, 1:dd + 1] = ents[ptr[rr]:ptr[rr] + dd]
+                rec[q, 1:dd + 1] = recs[ptr[rr]:ptr[rr] + dd]
+            out.append((LW, rows, ent, rec))
         width = np.where(long_, -1, width)
-        out.append((32, rows, ent, rec))
     for W in np.unique(width).tolist():
         if W < 0:
             continue
@@ -407,7 +415,7 @@ class HostLayout:
             if tp.kind == "constraint" and not direct:
                 if t in self.buckets:
                     for bi, bk in enumerate(self.buckets[t]["buckets"]):
-                        nth = bk["n"] * (32 if bk["d"] == 32 else 1)  # long rows: a warp per row
+                        nth = bk["n"] * (bk["d"] if bk["d"] >= 16 else 1)  # long rows: a (half) warp per row
                         for mode in (_lib.MODE_SET, _lib.MODE_CONS, _lib.MODE_JAC, _lib.MODE_HESS):
                             seg(mode, t, SEG_BUCKET + 16 * bi, nth)
                 elif t in self.fold_slots:

@@ -407,11 +407,16 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, m):
         L.append(f"    T.f[{i}] = A.f64 + {off}LL;")
     for i, off in enumerate(bk["ix_off"]):
         L.append(f"    T.ix[{i}] = A.i32 + {off}LL;")
-    L += [f"    const int q = (b - {cta0}) * {threads // 32} + tid / 32;",
-          "    const int lane = tid & 31;",
-          f"    if (q >= {n}) return;  // warp-uniform",
-          f"    const int r = __ldg(A.i32 + {bk['rows_off']}LL + q);",
-          f"    const int2 er = __ldg(reinterpret_cast<const int2*>(A.i32 + {bk['pair_off']}LL) + 32 * q + lane);",
+    LW = bk["d"]  # lanes per row: 32, or 16 (two rows per warp)
+    if LW == 32:
+        L += [f"    const int q = (b - {cta0}) * {threads // 32} + tid / 32;",
+              "    const int lane = tid & 31;",
+              f"    if (q >= {n}) return;  // warp-uniform"]
+    else:  # the second half of the last warp may redo row n-1 (same values, same slots)
+        L += [f"    const int q = min((b - {cta0}) * {threads // 16} + tid / 16, {n - 1});",
+              "    const int lane = tid & 15;"]
+    L += [f"    const int r = __ldg(A.i32 + {bk['rows_off']}LL + q);",
+          f"    const int2 er = __ldg(reinterpret_cast<const int2*>(A.i32 + {bk['pair_off']}LL) + {LW} * q + lane);",
           "    const int e = er.x, rc = er.y;",
           "    EXA_GRID_WAIT();"]
     if _bkt_release(threads):  # warp rows: release right after the wait
@@ -431,11 +436,17 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, m):
         L.append(f"      if (e >= 0 && rc >= 0) exa_bkout_T{t}<{int(want_j)}, {int(want_h)}>(e, xv, wrow, rc, A);")
     L.append("    }")
     if want_v:
-        L += ["    const int d = __popc(__ballot_sync(0xffffffffu, e >= 0));  // entries in lanes 1..d",
-              "    double acc = lane == 0 ? 0.0 + v : v;",
-              "    for (int s = 1; s <= d; ++s) {",
-              "      const double up = __shfl_up_sync(0xffffffffu, acc, 1);",
-              "      if (lane == s) acc = up + v;",
+        if LW == 32:
+            L += ["    const int d = __popc(__ballot_sync(0xffffffffu, e >= 0));  // entries in lanes 1..d",
+                  "    const int dm = d;"]
+        else:  # per half: own count d, loop to the larger of the two halves' counts
+            L += ["    const unsigned bal = __ballot_sync(0xffffffffu, e >= 0);",
+                  "    const int d = __popc((bal >> (tid & 16)) & 0xffffu);  // entries in lanes 1..d",
+                  "    const int dm = max(__popc(bal & 0xffffu), __popc(bal >> 16));"]
+        L += ["    double acc = lane == 0 ? 0.0 + v : v;",
+              "    for (int s = 1; s <= dm; ++s) {",
+              f"      const double up = __shfl_up_sync(0xffffffffu, acc, 1, {LW});",
+              "      if (lane == s && s <= d) acc = up + v;",
               "    }",
               "    if (lane == d) A.c[T.row_offset + r] = acc;"]
     L += ["    return;", "  }"]
@@ -464,7 +475,7 @@ def _kernel_source(layout, m, half, kname) -> str:
     for (t, kind, cta0, nrec, rpt) in segs:
         n_cta = (nrec + threads * rpt - 1) // (threads * rpt)
         b_ = [f"  if (b < {cta0 + n_cta}) {{"]
-        if kind & 15 == 4 and layout.buckets[t]["buckets"][kind >> 4]["d"] == 32:
+        if kind & 15 == 4 and layout.buckets[t]["buckets"][kind >> 4]["d"] >= 16:
             fn_body += _warp_row_source(layout, t, kind >> 4, cta0, n_cta, threads, m)
             continue
         if kind & 15 == 4:  # row bucket of augment-target block t: one thread per row

@@ -122,7 +122,8 @@ def test_domain_error_in_augment_row_sum():
 
 def _bucket_model(n_rows=40, seed=3):
     """Balance-like block with single-variable augments of two signs: rows
-    with 0, 1..8 and 9..31 contributions (every width class + warp rows),
+    with 0, 1..8, 9..15 and 16..31 contributions (every width class, half-warp
+    and warp rows),
     a base term with a variable (J/H written by the row thread) and
     duplicate variables across a row's augments."""
     core = ModelCore()
@@ -132,7 +133,9 @@ def _bucket_model(n_rows=40, seed=3):
     base = core.add_constraint(-field("d") - field("g") * x["b"] * x["b"],
                                DataTable({"d": rng.normal(size=n_rows), "g": rng.normal(size=n_rows),
                                           "b": rng.integers(0, 60, n_rows)}))
-    counts = np.concatenate([[0, 0, 1, 2, 3, 5, 8, 9, 15, 31], rng.integers(0, 9, n_rows - 10)])
+    # 9, 12, 15: three half-warp rows (odd count: the last warp's second half
+    # redoes a row); 31: a full warp row
+    counts = np.concatenate([[0, 0, 1, 2, 3, 5, 8, 9, 12, 15, 31], rng.integers(0, 9, n_rows - 11)])
     rows = np.repeat(np.arange(n_rows), counts)
     rng.shuffle(rows)
     half = rows.size // 2
@@ -148,7 +151,8 @@ def test_row_buckets_all_width_classes():
     lay = model.device_plan.layout
     assert lay.buckets, "expected the row-bucket layout"
     widths = {bk["d"] for info in lay.buckets.values() for bk in info["buckets"]}
-    assert 32 in widths and 8 in widths and 0 in widths
+    assert 32 in widths and 16 in widths and 8 in widths and 0 in widths
+    assert [bk["n"] for info in lay.buckets.values() for bk in info["buckets"] if bk["d"] == 16] == [3]
     _check_all(model)
     _check_all(model, seed=5)
 

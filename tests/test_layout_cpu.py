@@ -30,8 +30,8 @@ def _bucket_cons(model, x):
             rows = lay.i32[bk["rows_off"]:bk["rows_off"] + n]
             pairs = lay.i32[bk["pair_off"]:bk["pair_off"] + 2 * W * n] if W else np.zeros(0, np.int32)
             ent = pairs[0::2].reshape(W, n) if W else np.zeros((0, n), np.int32)
-            if W == 32:  # long rows: (n, 32) row-major, lane 0 = base
-                ent = pairs[0::2].reshape(n, 32).T
+            if W >= 16:  # long rows: (n, W) row-major, lane 0 = base
+                ent = pairs[0::2].reshape(n, W).T
             for q in range(n):
                 r = int(rows[q])
                 acc = 0.0 + float(vals[t][r])
