@@ -364,3 +364,31 @@ def test_back_to_back_sets_respect_dependencies(name):
         torch.cuda.synchronize()
         for got, r in zip(c, ref):
             assert np.array_equal(got.cpu().numpy().view(np.int64), r.view(np.int64))
+
+
+@pytest.mark.parametrize("name", ["case14_polar", "case5_strg_mp4_polar"])
+def test_numpy_callbacks_with_pinned_arrays(name):
+    """The separate numpy callbacks with page-locked arrays (``empty_pinned``:
+    direct D2H of the x-dependent ranges, constant runs filled on the host)
+    return the bits of the device path; outputs start as NaN."""
+    import torch
+
+    from paper_2510_12897_b200 import (empty_pinned, eval_callback_set, eval_constraints, eval_hessian,
+                                       eval_jacobian)
+
+    model, g = gpu_model(name)
+    x, y, w = g["x0"], g["y0"], float(g["w0"])
+    dev = [torch.empty(n, dtype=torch.float64, device="cuda")
+           for n in (model.ncon, model.plan.n_jac_slots, model.plan.n_hess_slots)]
+    eval_callback_set(model, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), w, *dev)
+    ref = [t.cpu().numpy() for t in dev]
+    xp, yp = empty_pinned(model.nvar), empty_pinned(model.ncon)
+    xp[:], yp[:] = x, y
+    out = [empty_pinned(n) for n in (model.ncon, model.plan.n_jac_slots, model.plan.n_hess_slots)]
+    for o in out:
+        o[:] = np.nan
+    eval_constraints(model, xp, out[0])
+    eval_jacobian(model, xp, out[1])
+    eval_hessian(model, xp, yp, w, out[2])
+    for a, r in zip(out, ref):
+        assert np.array_equal(a.view(np.int64), r.view(np.int64))
