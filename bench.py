@@ -136,6 +136,17 @@ def dist_setup():
     return ws, rank, local
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(model, x, y, w, seconds, workload):
     """Oracle port (numpy restatement of the reference) on 1 host core."""
     import numpy as np
@@ -153,7 +164,8 @@ def cpu_baseline(model, x, y, w, seconds, workload):
             break
     dt = time.perf_counter() - t0
     del np
-    return {"value": n / dt, "unit": "sets/s", "cores": 1, "kind": "port",
+    return {"value": n / dt, "unit": "sets/s", "cores": 1, "kind": "port", "cpu_model": _cpu_model(),
+            "os_cpu_count": os.cpu_count(),
             "sample": f"{n} sets of {workload} cons+jac+hess (numpy oracle, single thread, {dt:.1f} s)"}
 
 
@@ -187,7 +199,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "strong" if args.workload.startswith(("mp", "n1", "scen")) else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.workload, "sets_per_step": cores},
-        "cpu_baseline": {"value": value, "unit": "sets/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "sets/s", "cores": cores, "kind": "port", "cpu_model": _cpu_model(),
                          "sample": f"{sets} sets ({cores} processes x {args.steps} steps) of "
                                    f"{args.workload} cons+jac+hess, numpy restatement of the reference"},
         "e2e": {"value": value, "unit": "sets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
