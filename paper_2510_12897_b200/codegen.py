@@ -586,7 +586,7 @@ class PatternCode:
         pid = self.pid
         R = Gen.r
         # value-only function (row sums of augment-target rows, objective values)
-        out.append(f"__device__ __forceinline__ double exa_val_{pid}(const ExaTerm& T, int r, const ExaArgs& A, int rank) {{")
+        out.append(f"template <int LDH = 1>\n__device__ __forceinline__ double exa_val_{pid}(const ExaTerm& T, int r, const ExaArgs& A, int rank) {{")
         out.extend(pre)
         out.extend(value_lines)
         out.append(f"  return {R(value_root)};")
@@ -598,7 +598,7 @@ class PatternCode:
         # (light patterns) overlap their memory latency.
         # ``ro`` (default r): record index of the OUTPUT slots and the Hessian
         # weight, when the term's fields are read from a permuted copy (row buckets)
-        out.append(f"template <int MODE>\n__device__ __forceinline__ void exa_term_{pid}(const ExaTerm& T, int r, const ExaArgs& A, int rank, int ro = -1) {{")
+        out.append(f"template <int MODE, int LDH = 1>\n__device__ __forceinline__ void exa_term_{pid}(const ExaTerm& T, int r, const ExaArgs& A, int rank, int ro = -1) {{")
         out.append("  const int o = ro < 0 ? r : ro;")
         out.append("  double* __restrict__ Cout = A.c;")
         out.append("  double* __restrict__ Jout = A.J;")
@@ -807,7 +807,7 @@ def group_source(gid: int, entries: list, augs: list = ()) -> str:
     g.lines.extend(aug_late)
     args = ", ".join([f"const ExaTerm& T{m}" for m in range(M)] + [f"const ExaTerm& U{k}" for k in range(len(augs))])
     ranks = ", ".join(f"int rank{m}" for m in range(M))
-    out = [f"template <int MODE>\n__device__ __forceinline__ void exa_grp_{gid}({args}, int r, const ExaArgs& A, {ranks}) {{",
+    out = [f"template <int MODE, int LDH = 1>\n__device__ __forceinline__ void exa_grp_{gid}({args}, int r, const ExaArgs& A, {ranks}) {{",
            "  double* __restrict__ Cout = A.c;", "  double* __restrict__ Jout = A.J;",
            "  double* __restrict__ Hout = A.H;", "  int rank = rank0;"]
     out.extend(pre)

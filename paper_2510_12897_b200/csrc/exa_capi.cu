@@ -111,6 +111,7 @@ struct ExaPlan {
   int has_checks = 0;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern[EXA_NKERN] = {};
+  cudaKernel_t kern_batch = nullptr; /* strided-batch set kernel (parameters kept in L2), if the module has one */
   ExaWorkspace* dflt = nullptr;
   size_t bytes = 0;
   int pdl = 0;
@@ -528,6 +529,10 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
       p->grid[kid] = need < occ * n_sm ? need : occ * n_sm;
     }
   }
+  if (cudaLibraryGetKernel(&p->kern_batch, p->lib, "exa_k_setb_l") != cudaSuccess) {
+    cudaGetLastError();
+    p->kern_batch = nullptr;
+  }
   if ((rc = ws_alloc(p, &p->dflt))) return bail(rc);
   *out = p;
   return 0;
@@ -563,7 +568,8 @@ static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStrea
   attr[0].val.programmaticStreamSerializationAllowed = p->pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CU(cudaLaunchKernelExC(&cfg, (const void*)p->kern[kid], args));
+  const bool batch_kernel = nbatch > 1 && kid == 2 * EXA_MODE_SET + 1 && p->kern_batch;
+  CU(cudaLaunchKernelExC(&cfg, (const void*)(batch_kernel ? p->kern_batch : p->kern[kid]), args));
   return 0;
 }
 

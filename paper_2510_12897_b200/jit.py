@@ -177,6 +177,12 @@ __shared__ long long exa_tp_s[EXA_TRACE_NT][4];
 """
 
 _PREFETCH = r"""
+// per-record parameter loads (see _cache_hints): evict-first (LDH = 1) when a
+// launch evaluates one set; the strided-batch kernel (LDH = 0) reads the same
+// parameters for every set of the launch, so there they stay in L2.  LDH is a
+// template parameter of the generated functions; this is the default outside.
+constexpr int LDH = 1;
+#define EXA_LDP(p) (LDH ? __ldcs(p) : __ldg(p))
 // Bulk L2 prefetch of the gathered inputs: CTA b < n prefetches chunk b of x
 // (then of y).  The first random gathers of a set would otherwise miss L2
 // (the previous set used other buffers) and go to DRAM one 32-B sector at a
@@ -410,7 +416,7 @@ def _cache_hints(src: str) -> str:
         src = _ST_RE.sub(r"__stcs(&\1[\2], \3);", src)
     if LD_CS:
         for pat in _LD_RES:
-            src = pat.sub(r"__ldcs(\1)", src)
+            src = pat.sub(r"EXA_LDP(\1)", src)
     return src
 
 
@@ -453,9 +459,9 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, m):
     L += ["    double v = 0.0;",
           "    if (lane == 0) {"]
     if want_v:
-        L.append(f"      v = exa_val_{pid}(T, q, A, exa_rank(T, A));")
+        L.append(f"      v = exa_val_{pid}<LDH>(T, q, A, exa_rank(T, A));")
     if base_mode and layout.buckets[t]["base_k"]:
-        L.append(f"      exa_term_{pid}<{base_mode}>(T, q, A, exa_rank(T, A), r);")
+        L.append(f"      exa_term_{pid}<{base_mode}, LDH>(T, q, A, exa_rank(T, A), r);")
     L += ["    } else {",
           f"      const double xv = __ldg(A.x + (e & {(1 << 29) - 1} & ~(e >> 31)));"]
     if want_v:
@@ -499,7 +505,7 @@ def _kernel_source(layout, m, half, kname) -> str:
         bounds = f"{threads * V}, {max(1, min_blocks(threads) // V)}"
     segs = layout.mode_segments(kid)
     n_vb = sum((nrec + threads * rpt - 1) // (threads * rpt) for (_, _, _, nrec, rpt) in segs)
-    fn_body = [f"__device__ __forceinline__ void exa_vb_{kname}(const int b, const int tid, const ExaArgs& A) {{"]
+    fn_body = [f"template <int LDH>\n__device__ __forceinline__ void exa_vb_{kname}(const int b, const int tid, const ExaArgs& A) {{"]
     for (t, kind, cta0, nrec, rpt) in segs:
         n_cta = (nrec + threads * rpt - 1) // (threads * rpt)
         b_ = [f"  if (b < {cta0 + n_cta}) {{"]
@@ -541,7 +547,7 @@ def _kernel_source(layout, m, half, kname) -> str:
                     if want_v:
                         # base value first: its gathers issue with the entries' (a later
                         # re-load behind the base J/H stores would cost a round trip)
-                        b_.append(f"    const double base = exa_val_{layout.term_pid[t]}(T, q, A, exa_rank(T, A));")
+                        b_.append(f"    const double base = exa_val_{layout.term_pid[t]}<LDH>(T, q, A, exa_rank(T, A));")
                 for k in ks:
                     # pad entries (-1) gather x[0]: branch-free, selected away below
                     xv = f"__ldg(A.x + (e{k} & {(1 << 29) - 1} & ~(e{k} >> 31)))" if need_x else "0.0"
@@ -556,7 +562,7 @@ def _kernel_source(layout, m, half, kname) -> str:
                     # base term J/H after the entry gathers are issued (in-order issue:
                     # its stores wait on its own gather and would hold the others back)
                     if base_mode and info["base_k"]:
-                        b_.append(f"    exa_term_{layout.term_pid[t]}<{base_mode}>(T, q, A, exa_rank(T, A), r);")
+                        b_.append(f"    exa_term_{layout.term_pid[t]}<{base_mode}, LDH>(T, q, A, exa_rank(T, A), r);")
                     if want_v:
                         # reference order: zero-fill, base slice-add, augments in order (autodiff.py:573-580)
                         b_.append("    double acc = 0.0 + base;")
@@ -587,13 +593,13 @@ def _kernel_source(layout, m, half, kname) -> str:
             if rpt == 1:
                 b_.append(f"    const int r = (b - {cta0}) * {threads} + tid;")
                 b_.append(f"    if (r >= {nrec}) return;")
-                b_.append(f"    exa_grp_{t}<{_MODE_BITS[m]}>({tl}, r, A, {rl});")
+                b_.append(f"    exa_grp_{t}<{_MODE_BITS[m]}, LDH>({tl}, r, A, {rl});")
             else:
                 b_.append(f"    const int r0 = (b - {cta0}) * {threads * rpt} + tid;")
                 b_.append("#pragma unroll")
                 b_.append(f"    for (int q = 0; q < {rpt}; ++q) {{")
                 b_.append(f"      const int r = r0 + q * {threads};")
-                b_.append(f"      if (r < {nrec}) exa_grp_{t}<{_MODE_BITS[m]}>({tl}, r, A, {rl});")
+                b_.append(f"      if (r < {nrec}) exa_grp_{t}<{_MODE_BITS[m]}, LDH>({tl}, r, A, {rl});")
                 b_.append("    }")
         else:
             b_.append(f"    ExaTerm T; exa_init_T{t}(T, A);")
@@ -602,7 +608,7 @@ def _kernel_source(layout, m, half, kname) -> str:
                 b_.append("#pragma unroll")
                 b_.append(f"    for (int q = 0; q < {rpt}; ++q) {{")
                 b_.append(f"      const int r = r0 + q * {threads};")
-                b_.append(f"      if (r < {nrec}) exa_term_{layout.term_pid[t]}<{_MODE_BITS[m]}>(T, r, A, exa_rank(T, A));")
+                b_.append(f"      if (r < {nrec}) exa_term_{layout.term_pid[t]}<{_MODE_BITS[m]}, LDH>(T, r, A, exa_rank(T, A));")
                 b_.append("    }")
             else:  # fold rows are padded to whole warps: a warp never splits here
                 b_.append(f"    const int r = (b - {cta0}) * {threads} + tid;")
@@ -637,18 +643,22 @@ def _kernel_source(layout, m, half, kname) -> str:
                  f"  for (int b = (int)blockIdx.x + (int)gridDim.x * ((int)threadIdx.x / {threads}); b < {n_vb};"
                  f" b += (int)gridDim.x * {V}) {{",
                  "    EXA_TRACE_BEGIN();",
-                 f"    exa_vb_{kname}(b, tid, A);",
+                 f"    exa_vb_{kname}<@LDH@>(b, tid, A);",
                  f"    EXA_TRACE_END(b, tid, {threads});",
                  "  }"]
     else:
         body += ["  EXA_TRACE_BEGIN();",
-                 f"  exa_vb_{kname}((int)blockIdx.x, (int)threadIdx.x, A);",
+                 f"  exa_vb_{kname}<@LDH@>((int)blockIdx.x, (int)threadIdx.x, A);",
                  f"  EXA_TRACE_END((int)blockIdx.x, (int)threadIdx.x, {threads});"]
     # release the dependent grid only when this CTA's work is issued (an early
     # release lets later grids' waiting CTAs take the slots this grid needs)
     body.append("  EXA_GRID_RELEASE();")
     body.append("}")
-    return "\n".join(fn_body) + "\n" + "\n".join(body)
+    entry = "\n".join(body)
+    out = "\n".join(fn_body) + "\n" + entry.replace("@LDH@", "1")
+    if m == 0 and half == 1:  # strided-batch entry (exa_eval_set_batch): parameters stay in L2
+        out += "\n" + entry.replace("@LDH@", "0").replace(f" {kname}(", f" {kname.replace('_set_', '_setb_')}(", 1)
+    return out
 
 
 KERNEL_NAMES = ("exa_k_set", "exa_k_cons", "exa_k_jac", "exa_k_hess", "exa_k_objv", "exa_k_grad")
