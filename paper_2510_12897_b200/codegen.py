@@ -52,6 +52,11 @@ def _zero_const(v) -> bool:
 # drops the former in derivative space (see Gen.bin) and writes the latter as
 # +0.0 without loading the weight -- IEEE-equal values either way
 _DERIV_ZERO_ELISION = os.environ.get("EXA_EXACT_ZERO_SIGN", "0") != "1"
+# term-group members' multipliers (their own rows: each read once per set) are
+# loaded evict-first like the parameters (case13659 6.08 -> 5.99 us, MP96 39.4
+# -> 38.9); balance-row multipliers (augments, row buckets) are shared and
+# keep __ldg
+_WGT_CS = os.environ.get("EXA_WGT_CS", "1") == "1"
 
 
 class Arr:
@@ -742,8 +747,9 @@ def group_source(gid: int, entries: list, augs: list = ()) -> str:
         cnames.append(cn)
     for m, (pc, mem) in enumerate(entries):
         if pc.k:
+            ld = "EXA_LDP" if _WGT_CS else "__ldg"  # a member's own rows: each multiplier read once
             post.append(f"  const double wgt{m} = !(MODE & EXA_M_HESS) ? 0.0 : (T{m}.kind == EXA_OBJ) ? A.w"
-                        f" : __ldg(A.y + (T{m}.rows ? __ldg(T{m}.rows + r) : T{m}.row_offset + r));")
+                        f" : {ld}(A.y + (T{m}.rows ? __ldg(T{m}.rows + r) : T{m}.row_offset + r));")
     R = Gen.r
     # Stores are emitted as soon as their value is final (cons after the
     # value pass, J after the adjoint sweep, each Hessian column after its
