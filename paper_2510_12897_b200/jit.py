@@ -65,14 +65,15 @@ PREFETCH_CHUNK = int(os.environ.get("EXA_PREFETCH_CHUNK", "32768"))
 PDL = os.environ.get("EXA_PDL", "1") == "1"
 PDL_EARLY = os.environ.get("EXA_PDL_EARLY", "0") == "1"
 # row buckets' release point: 1 = once their entry gathers are issued, 2 = right
-# after the wait, 0 = CTA end; "auto" = 1 for one-wave sets (case13659 6.53 ->
-# 6.40 us), 0 for many-wave ones (MP96: 1 costs 2%, N-1 1%)
+# after the wait, 0 = CTA end; "auto" = 2 for one-wave sets (case13659: 0 ->
+# 1 6.53 -> 6.40 us; with the evict-first cache policy 2 beats 1, 5.99 ->
+# 5.92), 0 for many-wave ones (MP96: 1 costs 2%, N-1 1%)
 PDL_MID_BKT = os.environ.get("EXA_PDL_MID_BKT", "auto")
 
 
 def _bkt_release(threads: int) -> int:
     if PDL_MID_BKT == "auto":
-        return 1 if threads == 32 else 0
+        return 2 if threads == 32 else 0
     return int(PDL_MID_BKT)
 PDL_MID = int(os.environ.get("EXA_PDL_MID", "1"))
 ST_CS = os.environ.get("EXA_ST_CS", "1") == "1"  # evict-first stores of the c / J / H outputs
