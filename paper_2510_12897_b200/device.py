@@ -48,7 +48,11 @@ BUCKET_MAX_N = 48                      # at most this many distinct counts per b
 
 # Terms of one heavy pattern that share index columns (OPF: the 4 branch-flow
 # blocks) are evaluated by one thread per record (see codegen.group_source).
-GROUP_MAX = int(os.environ.get("EXA_GROUP_MAX", "2"))
+# terms per group: "auto" = 4 for sets that fit one wave of 32-thread CTAs
+# (OPF: all four flow blocks of a branch in one thread -- half the vm/va
+# gathers; case13659 5.92 -> 5.65 us with the evict-first cache policy), 2 for
+# many-wave sets (twice the threads hide more latency: MP96 39.4 vs 40.7 us)
+GROUP_MAX_ENV = os.environ.get("EXA_GROUP_MAX", "auto")
 ATTACH = os.environ.get("EXA_ATTACH", "1") == "1"  # light terms join heavy groups
 GROUP_RPT = int(os.environ.get("EXA_GROUP_RPT", "1"))  # records per thread of term groups (ILP)
 ATTACH_AUGS = os.environ.get("EXA_ATTACH_AUGS", "1") == "1"  # groups write aligned augments' J/H
@@ -367,7 +371,8 @@ class HostLayout:
         self.groups = []  # (pid, [term ids], members meta)
         self.group_of: dict = {}
         self.group_augs: dict = {}  # group id -> [(aug term, record offset, member, slot)]
-        if len(terms) <= META_CONST_MAX_TERMS and GROUP_MAX > 1:
+        self.group_max = self._group_max(terms)
+        if len(terms) <= META_CONST_MAX_TERMS and self.group_max > 1:
             self._make_groups(terms, descs)
             if ATTACH_AUGS:
                 self._attach_augs(terms)
@@ -518,6 +523,15 @@ class HostLayout:
         self.source = module_source(self.patterns, layout=self if self.specialised else None,
                                     threads=self.threads[1])
 
+    def _group_max(self, terms) -> int:
+        if GROUP_MAX_ENV != "auto":
+            return int(GROUP_MAX_ENV)
+        # threads of the set kernel with groups of 4 heavy terms (an estimate:
+        # light constraint terms counted as if ungrouped)
+        est = sum(tp.nrec / 4 if self.patterns[self.term_pid[t]].heavy else tp.nrec
+                  for t, tp in enumerate(terms) if tp.kind != "augment")
+        return 4 if choose_threads(int(est)) == 32 else 2
+
     def _make_groups(self, terms, descs):
         import hashlib
 
@@ -541,7 +555,7 @@ class HostLayout:
                 grp = [t0]
                 cols = set(hashes[t0])
                 for u in list(free):
-                    if len(grp) >= GROUP_MAX:
+                    if len(grp) >= self.group_max:
                         break
                     if cols & set(hashes[u]):
                         grp.append(u)
