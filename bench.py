@@ -360,7 +360,7 @@ def main():
         for r in range(RB):
             X = torch.stack([torch.from_numpy(eval_inputs(model, 100 + r * NB + k)[0]) for k in range(NB)]).to(dev)
             Y = torch.stack([torch.from_numpy(eval_inputs(model, 100 + r * NB + k)[1]) for k in range(NB)]).to(dev)
-            bb.append((DevicePlan(model, local), X, Y,
+            bb.append((DevicePlan(model, local, group_max=2), X, Y,
                        torch.empty(NB, model.ncon, dtype=torch.float64, device=dev),
                        torch.empty(NB, model.plan.n_jac_slots, dtype=torch.float64, device=dev),
                        torch.empty(NB, model.plan.n_hess_slots, dtype=torch.float64, device=dev)))

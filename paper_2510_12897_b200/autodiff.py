@@ -56,6 +56,22 @@ def _dplan(model):
     return dp
 
 
+def _dplan_batch(model):
+    """Device plan for strided batches: a batch is many waves, where term
+    groups of two beat the one-wave grouping of four (case13659 x8: 73% vs
+    64% of the HBM peak), so single-wave models get a second plan."""
+    dp = _dplan(model)
+    if dp.layout.group_max <= 2:
+        return dp
+    bp = getattr(model, "_exa_batch_plan", None)
+    if bp is None or bp.device != dp.device:
+        from .device import DevicePlan
+
+        bp = DevicePlan(model, dp.device, group_max=2)
+        model._exa_batch_plan = bp
+    return bp
+
+
 def _is_cuda(a) -> bool:
     return getattr(a, "is_cuda", False)
 
@@ -320,7 +336,7 @@ def eval_callback_set_batch(model, X, Y, obj_weight: float, C_out, J_out, H_out)
                        (J_out, plan.n_jac_slots, "J_out"), (H_out, plan.n_hess_slots, "H_out")):
         if not _is_cuda(a) or a.dtype != torch.float64 or not a.is_contiguous() or tuple(a.shape) != (k, n):
             raise ValueError(f"{what} must be a contiguous float64 CUDA tensor of shape ({k}, {n})")
-    dp = _dplan(model)
+    dp = _dplan_batch(model) if k > 1 else _dplan(model)
     s = C.c_void_p(torch.cuda.current_stream(X.device).cuda_stream)
     _lib.check(dp._lib.exa_eval_set_batch(dp.handle, None, k, X.data_ptr(), Y.data_ptr(), float(obj_weight),
                                           C_out.data_ptr(), J_out.data_ptr(), H_out.data_ptr(), s),

@@ -282,9 +282,10 @@ def _bucket_layout(base_tp, augs, nvar):
 class HostLayout:
     """Everything the device needs for one plan, built on the host only."""
 
-    def __init__(self, plan):
+    def __init__(self, plan, group_max: int | None = None):
         self.plan = plan
         self.env_sig = (THREADS_ENV, THREADS_HEAVY, PDL)
+        self.group_max_req = group_max
         terms = plan.obj_terms + plan.con_terms
         self.terms = terms
         n_obj = len(plan.obj_terms)
@@ -524,6 +525,8 @@ class HostLayout:
                                     threads=self.threads[1])
 
     def _group_max(self, terms) -> int:
+        if self.group_max_req is not None:
+            return int(self.group_max_req)
         if GROUP_MAX_ENV != "auto":
             return int(GROUP_MAX_ENV)
         # threads of the set kernel with groups of 4 heavy terms (an estimate:
@@ -709,23 +712,36 @@ class HostLayout:
         return ptr, ent
 
 
-def host_layout(plan) -> HostLayout:
-    lay = getattr(plan, "_exa_layout", None)
-    if lay is None or lay.env_sig != (THREADS_ENV, THREADS_HEAVY, PDL):
-        lay = HostLayout(plan)
-        plan._exa_layout = lay
-    return lay
+def host_layout(plan, group_max: int | None = None) -> HostLayout:
+    """The plan's device layout (cached on the plan); ``group_max`` overrides
+    the automatic term-group size (the strided-batch plan uses 2)."""
+    if group_max is None:
+        lay = getattr(plan, "_exa_layout", None)
+        if lay is None or lay.env_sig != (THREADS_ENV, THREADS_HEAVY, PDL):
+            lay = HostLayout(plan)
+            plan._exa_layout = lay
+        return lay
+    cache = plan.__dict__.setdefault("_exa_layouts", {})
+    key = (THREADS_ENV, THREADS_HEAVY, PDL, group_max)
+    if key not in cache:
+        cache[key] = HostLayout(plan, group_max)
+    return cache[key]
 
 
 def precompile(plan) -> bytes:
-    """JIT (or fetch from cache) the module for a host plan; no GPU needed."""
-    return compile_module(host_layout(plan).source)
+    """JIT (or fetch from cache) the module for a host plan -- and the
+    strided-batch variant when the plan groups more than two terms; no GPU
+    needed."""
+    lay = host_layout(plan)
+    if lay.specialised and lay.group_max > 2:
+        compile_module(host_layout(plan, 2).source)
+    return compile_module(lay.source)
 
 
 class DevicePlan:
     """The model's plan resident on one GPU, with its compiled kernels."""
 
-    def __init__(self, model, device=None):
+    def __init__(self, model, device=None, group_max: int | None = None):
         import torch
 
         if not torch.cuda.is_available():
@@ -734,7 +750,7 @@ class DevicePlan:
         plan = model.plan
         self.model = model
         self.plan = plan
-        lay = host_layout(plan)
+        lay = host_layout(plan, group_max)
         self.layout = lay
         self.patterns = lay.patterns
         self.has_checks = lay.has_checks
