@@ -24,10 +24,13 @@
  *  - results are run-to-run bitwise deterministic: no floating-point atomics,
  *    fixed reduction orders equal to the reference's;
  *  - status: 0 ok, < 0 invalid argument / CUDA failure (exa_last_error());
- *  - a plan is immutable after creation; concurrent evaluation on distinct
- *    streams needs distinct workspaces (exa_workspace_create) for obj/grad and
- *    domain-error reporting; cons/jac/hess/set need no workspace state when
- *    the plan has no domain-checked ops.
+ *  - a plan is immutable after creation and shareable across threads
+ *    (reference core.py:301-305); all mutable evaluation state (obj/grad
+ *    scratch, the domain-error word, host-path staging, the light kernels'
+ *    aux stream) lives in an ExaWorkspace.  A workspace serves one evaluation
+ *    at a time: concurrent callers pass one workspace each
+ *    (exa_workspace_create); NULL selects the plan's default workspace, for
+ *    single-threaded callers.  The Python layer gives every thread its own.
  */
 #ifndef EXA_H
 #define EXA_H

@@ -86,9 +86,15 @@ class _Stage:
         self.back: list = []
         self.keep: list = []
 
+    def _same_device(self, a):
+        if a.device != self.dev:
+            raise ValueError(f"tensor on {a.device}, but the model's device plan is on {self.dev}"
+                             " (model.to_device(ordinal) re-lowers it)")
+
     def inp(self, a):
         torch = self.torch
         if _is_cuda(a):
+            self._same_device(a)
             if a.dtype != torch.float64 or not a.is_contiguous():
                 a = a.to(torch.float64).contiguous()
             self.keep.append(a)
@@ -100,6 +106,7 @@ class _Stage:
     def out(self, a, n):
         torch = self.torch
         if _is_cuda(a):
+            self._same_device(a)
             if a.dtype != torch.float64 or not a.is_contiguous():
                 raise ValueError("device output buffers must be contiguous float64 CUDA tensors")
             return a.data_ptr()
@@ -141,7 +148,7 @@ def _raise_domain(dp, ws_stream, callback: str):
     if not dp.has_checks:
         return
     rank, instr, rec = C.c_int64(), C.c_int32(), C.c_int64()
-    rc = _lib.check(dp._lib.exa_domain_error(dp.handle, None, ws_stream, C.byref(rank), C.byref(instr),
+    rc = _lib.check(dp._lib.exa_domain_error(dp.handle, dp.workspace(), ws_stream, C.byref(rank), C.byref(instr),
                                              C.byref(rec)), "domain_error")
     if rc != 1:
         return
@@ -168,7 +175,7 @@ def eval_objective(model, x) -> float:
     xp = st.inp(x)
     out = st.torch.empty(1, dtype=st.torch.float64, device=st.dev)
     s = st.stream()
-    _lib.check(dp._lib.exa_eval_obj(dp.handle, None, xp, out.data_ptr(), s), "eval_objective")
+    _lib.check(dp._lib.exa_eval_obj(dp.handle, dp.workspace(), xp, out.data_ptr(), s), "eval_objective")
     _raise_domain(dp, s, "obj")
     return float(out.item())
 
@@ -205,7 +212,7 @@ def _host_call(dp, name: str, callback: str, *args) -> None:
         else:
             conv.append(a)
     s = C.c_void_p(stream.cuda_stream)
-    _lib.check(getattr(dp._lib, name)(dp.handle, None, *conv, s), name)
+    _lib.check(getattr(dp._lib, name)(dp.handle, dp.workspace(), *conv, s), name)
     _raise_domain(dp, s, callback)
     stream.synchronize()
 
@@ -218,7 +225,7 @@ def eval_gradient(model, x, out_g) -> None:
     st = _Stage(dp)
     xp, gp = st.inp(x), st.out(out_g, model.nvar)
     s = st.stream()
-    _lib.check(dp._lib.exa_eval_grad(dp.handle, None, xp, gp, s), "eval_gradient")
+    _lib.check(dp._lib.exa_eval_grad(dp.handle, dp.workspace(), xp, gp, s), "eval_gradient")
     _raise_domain(dp, s, "grad")
     st.finish()
 
@@ -235,7 +242,7 @@ def eval_constraints(model, x, out_c) -> None:
     st = _Stage(dp)
     xp, cp = st.inp(x), st.out(out_c, model.ncon)
     s = st.stream()
-    _lib.check(dp._lib.exa_eval_cons(dp.handle, None, xp, cp, s), "eval_constraints")
+    _lib.check(dp._lib.exa_eval_cons(dp.handle, dp.workspace(), xp, cp, s), "eval_constraints")
     _raise_domain(dp, s, "cons")
     st.finish()
 
@@ -256,7 +263,7 @@ def eval_jacobian(model, x, out_vals) -> None:
     st = _Stage(dp)
     xp, jp = st.inp(x), st.out(out_vals, n)
     s = st.stream()
-    _lib.check(dp._lib.exa_eval_jac(dp.handle, None, xp, jp, s), "eval_jacobian")
+    _lib.check(dp._lib.exa_eval_jac(dp.handle, dp.workspace(), xp, jp, s), "eval_jacobian")
     _raise_domain(dp, s, "jac")
     st.finish()
 
@@ -292,7 +299,7 @@ def eval_hessian(model, x, mult, obj_weight: float, out_vals) -> None:
     yp = st.inp(mult) if model.ncon else 0
     hp = st.out(out_vals, n)
     s = st.stream()
-    _lib.check(dp._lib.exa_eval_hess(dp.handle, None, xp, yp, float(obj_weight), hp, s), "eval_hessian")
+    _lib.check(dp._lib.exa_eval_hess(dp.handle, dp.workspace(), xp, yp, float(obj_weight), hp, s), "eval_hessian")
     _raise_domain(dp, s, "hess")
     st.finish()
 
@@ -320,7 +327,7 @@ def eval_callback_set(model, x, mult, obj_weight: float, out_c, out_jac, out_hes
     jp = st.out(out_jac, plan.n_jac_slots)
     hp = st.out(out_hess, plan.n_hess_slots)
     s = st.stream()
-    _lib.check(dp._lib.exa_eval_set(dp.handle, None, xp, yp, float(obj_weight), cp, jp, hp, s), "eval_set")
+    _lib.check(dp._lib.exa_eval_set(dp.handle, dp.workspace(), xp, yp, float(obj_weight), cp, jp, hp, s), "eval_set")
     _raise_domain(dp, s, "set")
     st.finish()
 
@@ -338,7 +345,7 @@ def eval_callback_set_batch(model, X, Y, obj_weight: float, C_out, J_out, H_out)
             raise ValueError(f"{what} must be a contiguous float64 CUDA tensor of shape ({k}, {n})")
     dp = _dplan_batch(model) if k > 1 else _dplan(model)
     s = C.c_void_p(torch.cuda.current_stream(X.device).cuda_stream)
-    _lib.check(dp._lib.exa_eval_set_batch(dp.handle, None, k, X.data_ptr(), Y.data_ptr(), float(obj_weight),
+    _lib.check(dp._lib.exa_eval_set_batch(dp.handle, dp.workspace(), k, X.data_ptr(), Y.data_ptr(), float(obj_weight),
                                           C_out.data_ptr(), J_out.data_ptr(), H_out.data_ptr(), s),
                "eval_set_batch")
 

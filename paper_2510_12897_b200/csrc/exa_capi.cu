@@ -84,6 +84,9 @@ struct ExaWorkspace {
   /* pinned host staging for pageable callers: x, mult | c, J ranges, H ranges */
   double* hstage = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
+  /* guards the lazy staging allocation (a workspace serves one evaluation at
+     a time; concurrent callers use one workspace each) */
+  std::mutex mu;
 };
 
 struct ExaPlan {
@@ -159,10 +162,12 @@ __global__ void exa_obj_leaves(const double* __restrict__ V, const int64_t* __re
 }
 
 // The pairwise tree above the leaves plus the Python-level `total += s_t`
-// accumulation over objective blocks, replayed by one thread.
+// accumulation over objective blocks, replayed by one thread.  The program's
+// stack depth is validated on the host at plan creation (prog_depth).
+#define EXA_OBJ_STACK 96
 __global__ void exa_obj_combine(const int64_t* __restrict__ prog, int n_prog,
                                 const double* __restrict__ leafsum, double* __restrict__ out) {
-  double stack[96];
+  double stack[EXA_OBJ_STACK];
   int sp = 0;
   double total = 0.0;
   for (int p = 0; p < n_prog; ++p) {
@@ -180,9 +185,30 @@ __global__ void exa_obj_combine(const int64_t* __restrict__ prog, int n_prog,
       case OP_TOTAL_ADD: total = total + stack[--sp]; break;
       default: break;
     }
-    if (sp >= 96) sp = 95;  // malformed program guard
   }
   *out = total;
+}
+
+// Stack depth of an objective combine program, or -1 if it is malformed
+// (unknown opcode, pop from an empty stack, leaf index out of range).
+static int prog_depth(const int64_t* prog, int n_prog, int n_leaves) {
+  int sp = 0, mx = 0;
+  for (int p = 0; p < n_prog; ++p) {
+    const int64_t op = prog[3 * p], a = prog[3 * p + 1];
+    switch ((int)op) {
+      case OP_LEAF:
+        if (a < 0 || a >= n_leaves) return -1;
+        ++sp;
+        break;
+      case OP_CONST: ++sp; break;
+      case OP_ADD: if (sp < 2) return -1; --sp; break;
+      case OP_ZERO_PLUS: if (sp < 1) return -1; break;
+      case OP_TOTAL_ADD: if (sp < 1) return -1; --sp; break;
+      default: return -1;
+    }
+    if (sp > mx) mx = sp;
+  }
+  return mx;
 }
 
 // g[v] = ((0 + B_1) + B_2) + ..., B_k = sequential bincount sum of group k.
@@ -502,6 +528,12 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
 
   p->n_leaves = d->n_leaves;
   p->n_prog = d->n_prog;
+  {
+    const int depth = d->n_prog ? prog_depth(d->obj_prog, d->n_prog, d->n_leaves) : 0;
+    if (depth < 0) return bail(fail("objective combine program is malformed"));
+    if (depth > EXA_OBJ_STACK)
+      return bail(fail("objective combine program needs a stack of %d > %d entries", depth, EXA_OBJ_STACK));
+  }
   if ((rc = dev_upload(&p->leaves, d->leaves, (size_t)d->n_leaves * 2))) return bail(rc);
   if ((rc = dev_upload(&p->prog, d->obj_prog, (size_t)d->n_prog * 3))) return bail(rc);
   if (d->grad_ptr) {
@@ -607,8 +639,23 @@ static int reset_err(ExaPlan* p, ExaWorkspace* w, cudaStream_t st) {
   return 0;
 }
 
+// Launches go to the plan's device: make it current for the call (and restore
+// the caller's device after), so a caller whose current device differs gets
+// the plan's kernels on the plan's device instead of a launch error.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 #define EXA_PROLOGUE()                                      \
   if (!p) return fail("null plan");                         \
+  DeviceGuard dguard_(p->device);                           \
   ExaWorkspace* w = ws ? ws : p->dflt;                      \
   cudaStream_t st = (cudaStream_t)stream;                   \
   ExaArgs A;                                                \
@@ -768,7 +815,9 @@ static std::vector<Range> d2h_ranges(const ExaPlan* p, const ExaWorkspace* w, do
 static int host_eval(ExaPlan* p, ExaWorkspace* ws, int mode, const double* x, const double* mult, double w_obj,
                      double* c, double* jac, double* hess, cudaStream_t st) {
   if (!p) return fail("null plan");
+  DeviceGuard dguard(p->device);
   ExaWorkspace* w = ws ? ws : p->dflt;
+  std::unique_lock<std::mutex> lazy(w->mu);
   if (!w->dx) {  // first use: device staging sized for this plan
     CU(cudaSetDevice(p->device));
     CU(cudaMalloc((void**)&w->dx, (p->nvar > 0 ? p->nvar : 1) * sizeof(double)));
@@ -788,6 +837,7 @@ static int host_eval(ExaPlan* p, ExaWorkspace* ws, int mode, const double* x, co
     CU(cudaHostAlloc((void**)&w->hstage, (p->nvar + 2 * p->ncon + p->n_jac + p->n_hess + 1) * sizeof(double),
                      cudaHostAllocDefault));
   }
+  lazy.unlock();
   const double* xs = x;
   const double* ys = mult;
   if (pg_in) {  // pageable inputs: host threads copy them into pinned staging, then one DMA each

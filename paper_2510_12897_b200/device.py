@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 
 import numpy as np
 
@@ -828,6 +829,28 @@ class DevicePlan:
         self.handle = handle
         self._lib = lib
         self.device_bytes = int(lay.f64.nbytes + lay.i32.nbytes)
+        self._tls = threading.local()
+        self._ws_lock = threading.Lock()
+        self._workspaces: list = []
+
+    def workspace(self) -> C.c_void_p:
+        """The calling thread's workspace (objective / gradient scratch,
+        domain-error word, host-path staging, the aux stream of the light
+        kernels).  The plan itself is immutable, so one model is shareable
+        across threads (reference ``core.py:301-305``): every Python thread
+        evaluates through its own workspace, created on first use and
+        destroyed with the plan."""
+        ws = getattr(self._tls, "ws", None)
+        if ws is None:
+            import torch
+
+            ws = C.c_void_p()
+            with torch.cuda.device(self.device):
+                _lib.check(self._lib.exa_workspace_create(self.handle, C.byref(ws)), "exa_workspace_create")
+            with self._ws_lock:
+                self._workspaces.append(ws)
+            self._tls.ws = ws
+        return ws
 
     def info(self):
         b, r = C.c_int64(), C.c_int32()
@@ -842,6 +865,8 @@ class DevicePlan:
         h = getattr(self, "handle", None)
         if h is not None and h.value:
             try:
+                for ws in getattr(self, "_workspaces", ()):
+                    self._lib.exa_workspace_destroy(ws)
                 self._lib.exa_plan_destroy(h)
             except Exception:  # pragma: no cover - interpreter shutdown
                 pass

@@ -93,6 +93,34 @@ def algorithmic_bytes(model) -> dict:
     return parts
 
 
+def algorithmic_bytes_mode(model, mode: str) -> int:
+    """Compulsory bytes of ONE callback (``set``, ``cons``, ``jac``, ``hess``):
+    x once, the multipliers for the Hessian, the parameters of the terms the
+    callback evaluates (cons: every constraint-side term; jac: those with
+    variables; hess: every term with variables, objective included), and
+    the callback's own output."""
+    if mode == "set":
+        return algorithmic_bytes(model)["total"]
+    plan = model.plan
+
+    def params(terms):
+        n = 0
+        for tp in terms:
+            n_idx = len(tp.tape.index_names) + (1 if tp.kind == "augment" else 0)
+            n += tp.nrec * (8 * len(tp.tape.field_names) + 4 * n_idx)
+        return n
+
+    b = 8 * model.nvar
+    if mode == "cons":
+        return b + params(plan.con_terms) + 8 * model.ncon
+    if mode == "jac":
+        return b + params([tp for tp in plan.con_terms if tp.tape.k]) + 8 * plan.n_jac_slots
+    if mode == "hess":
+        return (b + 8 * model.ncon + params([tp for tp in plan.obj_terms + plan.con_terms if tp.tape.k])
+                + 8 * plan.n_hess_slots)
+    raise ValueError(mode)
+
+
 def bench_models_for_precompile():
     """Host plans whose kernel modules build() pre-compiles (no GPU needed)."""
     out = []

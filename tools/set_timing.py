@@ -16,13 +16,14 @@ import torch
 
 from paper_2510_12897_b200 import _lib, jit
 from paper_2510_12897_b200.device import DevicePlan
-from paper_2510_12897_b200.workloads import build_workload, eval_inputs, model_summary
+from paper_2510_12897_b200.workloads import algorithmic_bytes_mode, build_workload, eval_inputs, model_summary
 
 name = sys.argv[1] if len(sys.argv) > 1 else "case13659"
 mode = sys.argv[2] if len(sys.argv) > 2 else "set"
 model = build_workload(name, lower_to_gpu=False)
 bps = model_summary(model)["bytes_per_set"]
-R = int(os.environ.get("EXA_R", "0")) or max(2, int(np.ceil(2 * 126 * 2**20 / bps)))
+mode_bytes = algorithmic_bytes_mode(model, mode)  # this callback's own compulsory bytes
+R = int(os.environ.get("EXA_R", "0")) or max(3, int(np.ceil(2 * 126 * 2**20 / mode_bytes)))
 dev = torch.device("cuda", 0)
 t0 = time.time()
 plans = [DevicePlan(model, 0) for _ in range(R)]
@@ -76,6 +77,6 @@ with torch.cuda.stream(st):
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / (5 * S * R)
 info = plans[0].info()
-print(json.dumps({"workload": name, "mode": mode, "bytes": bps, "R": R, "threads": plans[0].layout.threads[1], "minb": jit.MINB_ENV,
-                  "sincos": jit.SINCOS_IMPL, "persist": jit.PERSIST, "pdl": jit.PDL, "env": {k: v for k, v in os.environ.items() if k.startswith("EXA_")}, "us_per_set": us, "GBps": bps / us / 1e3,
+print(json.dumps({"workload": name, "mode": mode, "bytes": mode_bytes, "set_bytes": bps, "R": R, "threads": plans[0].layout.threads[1], "minb": jit.MINB_ENV,
+                  "sincos": jit.SINCOS_IMPL, "persist": jit.PERSIST, "pdl": jit.PDL, "env": {k: v for k, v in os.environ.items() if k.startswith("EXA_")}, "us_per_set": us, "GBps": mode_bytes / us / 1e3,
                   "regs": info["regs_set_kernel"], "ctas": info["ctas"], "jit_s": tjit}), flush=True)
