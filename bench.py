@@ -14,7 +14,17 @@ configs (default case13659) every rank evaluates its own scenario stream (weak
 scaling, no data-path collective); for the batched configs
 (``--workload mp96_case1354`` / ``n1_case2000``) each rank evaluates its
 period / instance shard of ONE instance (strong scaling; cons/jac/hess need
-no collective).  Time = max over ranks.
+no collective).  Time = max over ranks.  At N > 1 the default run also
+measures the sharded MP96 and N-1 configs (``sharded`` key): their sets/s
+over the N ranks, one ``ShardComm.exchange`` (NCCL P2P halo of the borrowed
+variables) and one objective reduction (NCCL all-gather), max over ranks.
+
+Extra keys (not the headline): ``zero_sign`` (the other code-generation mode
+of the same kernel), ``latency`` (one isolated set, no neighbour to overlap
+with), ``callbacks`` (separate cons / jac / hess / obj / grad kernels),
+``compressed`` (the solver's compressed J/H values), ``batched`` (several
+independent sets per launch), ``parity`` (replica 0 against the CPU oracle
+at the same point, in the cpu_baseline leg).
 """
 
 from __future__ import annotations
@@ -33,6 +43,7 @@ sys.path.insert(0, str(ROOT))
 
 L2_BYTES = 126 * 2**20
 METRIC = "AC-OPF callback sets/sec (cons+jac+hess) at 13659-bus; % of HBM roofline"
+SHARDED = ("mp", "n1", "scen")
 
 
 def parse():
@@ -46,6 +57,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="headline and e2e only")
+    ap.add_argument("--sharded-legs", action="store_true", help="run the sharded MP96 / N-1 legs at N = 1 too")
     return ap.parse_args()
 
 
@@ -58,15 +71,21 @@ def peaks():
 
 
 def profiled_traffic(workload):
-    """dram bytes per launch of the set kernel from the committed ncu summary."""
-    for p in sorted((ROOT / "profiles").glob("*ncu_summary*.json"), reverse=True):
+    """DRAM bytes per launch of the set kernel from the committed ncu summary
+    (steady state under buffer rotation when available)."""
+    best = None
+    for p in sorted((ROOT / "profiles").glob("*ncu*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
         except Exception:
             continue
-        if d.get("workload") == workload and d.get("dram_bytes_per_launch"):
-            return float(d["dram_bytes_per_launch"]), p.name
-    return None, None
+        if d.get("workload") != workload:
+            continue
+        if d.get("steady_state_dram_bytes_per_set"):
+            return float(d["steady_state_dram_bytes_per_set"]), p.name
+        if best is None and d.get("dram_bytes_per_launch"):
+            best = (float(d["dram_bytes_per_launch"]), p.name)
+    return best if best else (None, None)
 
 
 class ClockSampler:
@@ -147,26 +166,52 @@ def _cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline(model, x, y, w, seconds, workload):
-    """Oracle port (numpy restatement of the reference) on 1 host core."""
+def _pin_core0():
+    """numpy's callbacks are single-threaded -- pin to one core."""
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+        return sorted(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return None
+
+
+def cpu_baseline(model, x, y, w, seconds, workload, gpu_out=None):
+    """Oracle port (numpy restatement of the reference, pinned bit-exact to
+    its goldens) on ONE host core, pinned like `taskset -c 0`.  It also checks
+    the GPU's replica-0 outputs at the same point (``parity``)."""
     import numpy as np
 
     from oracle import tape_oracle as O
+    from oracle.parity import strict_violations, zero_sign_mismatches
 
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    O.eval_set(model.plan, x, y, w)  # warm
-    n = 0
-    t0 = time.perf_counter()
-    while True:
-        O.eval_set(model.plan, x, y, w)
-        n += 1
-        if time.perf_counter() - t0 >= seconds or n >= 400:
-            break
-    dt = time.perf_counter() - t0
-    del np
-    return {"value": n / dt, "unit": "sets/s", "cores": 1, "kind": "port", "cpu_model": _cpu_model(),
-            "os_cpu_count": os.cpu_count(),
-            "sample": f"{n} sets of {workload} cons+jac+hess (numpy oracle, single thread, {dt:.1f} s)"}
+    before = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    pinned = _pin_core0()
+    try:
+        ref = O.eval_set(model.plan, x, y, w)  # warm, and the parity reference
+        n = 0
+        t0 = time.perf_counter()
+        while True:
+            O.eval_set(model.plan, x, y, w)
+            n += 1
+            if time.perf_counter() - t0 >= seconds or n >= 400:
+                break
+        dt = time.perf_counter() - t0
+    finally:
+        if before is not None:
+            os.sched_setaffinity(0, before)
+    out = {"value": n / dt, "unit": "sets/s", "cores": 1, "kind": "port", "cpu_model": _cpu_model(),
+           "os_cpu_count": os.cpu_count(), "affinity": pinned,
+           "sample": f"{n} sets of {workload} cons+jac+hess (numpy oracle, single thread pinned to one core, "
+                     f"{dt:.1f} s)"}
+    parity = None
+    if gpu_out is not None:
+        parity = {"point": "eval_inputs(model, 0) = bench replica 0", "rtol": 1e-12}
+        for label, a, r in zip(("cons", "jac", "hess"), gpu_out, ref):
+            parity[label] = {"n": int(a.size), "strict_violations": int(strict_violations(a, r).size),
+                             "ieee_unequal": int(np.count_nonzero(a != r)),
+                             "zero_sign_mismatch": zero_sign_mismatches(a, r)}
+    return out, parity
 
 
 def run_reference(args):
@@ -197,7 +242,8 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "strong" if args.workload.startswith(("mp", "n1", "scen")) else "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.workload.startswith(SHARDED) else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.workload, "sets_per_step": cores},
         "cpu_baseline": {"value": value, "unit": "sets/s", "cores": cores, "kind": "port", "cpu_model": _cpu_model(),
                          "sample": f"{sets} sets ({cores} processes x {args.steps} steps) of "
@@ -225,6 +271,258 @@ def info_batchable(dp) -> bool:
     return bool(dp.layout.specialised) and not dp.has_checks
 
 
+# ---------------------------------------------------------------------------
+# GPU helpers
+# ---------------------------------------------------------------------------
+
+def replicas(model, R, local, seed0, **plan_kw):
+    """R full working sets: a device plan (parameters) plus x, y, c, J, H each."""
+    import torch
+
+    from paper_2510_12897_b200.device import DevicePlan
+    from paper_2510_12897_b200.workloads import eval_inputs
+
+    dev = torch.device("cuda", local)
+    plans, bufs = [], []
+    for r in range(R):
+        plans.append(DevicePlan(model, local, **plan_kw))
+        x, y, w = eval_inputs(model, seed=seed0 + r)
+        bufs.append({
+            "x": torch.from_numpy(x).to(dev), "y": torch.from_numpy(y).to(dev), "w": w,
+            "c": torch.empty(model.ncon, dtype=torch.float64, device=dev),
+            "J": torch.empty(model.plan.n_jac_slots, dtype=torch.float64, device=dev),
+            "H": torch.empty(model.plan.n_hess_slots, dtype=torch.float64, device=dev),
+            "g": torch.empty(model.nvar, dtype=torch.float64, device=dev),
+            "f": torch.empty(1, dtype=torch.float64, device=dev),
+        })
+    return plans, bufs
+
+
+def launcher(lib, plans, bufs, stream, mode="set"):
+    import ctypes as C
+
+    sh = C.c_void_p(stream.cuda_stream)
+    R = len(plans)
+
+    def launch(i):
+        b, p = bufs[i % R], plans[i % R].handle
+        if mode == "set":
+            rc = lib.exa_eval_set(p, None, b["x"].data_ptr(), b["y"].data_ptr(), b["w"], b["c"].data_ptr(),
+                                  b["J"].data_ptr(), b["H"].data_ptr(), sh)
+        elif mode == "cons":
+            rc = lib.exa_eval_cons(p, None, b["x"].data_ptr(), b["c"].data_ptr(), sh)
+        elif mode == "jac":
+            rc = lib.exa_eval_jac(p, None, b["x"].data_ptr(), b["J"].data_ptr(), sh)
+        elif mode == "hess":
+            rc = lib.exa_eval_hess(p, None, b["x"].data_ptr(), b["y"].data_ptr(), b["w"], b["H"].data_ptr(), sh)
+        elif mode == "obj":
+            rc = lib.exa_eval_obj(p, None, b["x"].data_ptr(), b["f"].data_ptr(), sh)
+        elif mode == "grad":
+            rc = lib.exa_eval_grad(p, None, b["x"].data_ptr(), b["g"].data_ptr(), sh)
+        else:
+            raise ValueError(mode)
+        if rc:
+            raise RuntimeError(lib.exa_last_error().decode())
+
+    return launch
+
+
+def graph_us(launch, n, stream, dev, reps=5):
+    """Mean device time per launch of a CUDA graph of n launches (CUDA events on
+    the launching stream, after a warm replay)."""
+    import torch
+
+    with torch.cuda.stream(stream):
+        for i in range(min(n, 16)):
+            launch(i)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(n):
+                launch(i)
+        g.replay()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) * 1e3 / (reps * n)
+
+
+def isolated_latency_us(launch, stream, dev, n=40):
+    """One set with nothing before or after it on the stream (an IPM evaluates
+    one set per iteration): median of per-launch CUDA-event intervals."""
+    import torch
+
+    out = []
+    for i in range(n):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            launch(i)
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        out.append(e0.elapsed_time(e1) * 1e3)
+    return statistics.median(out[5:])
+
+
+def sharded_leg(name, rank, ws, local, n_sets=8, steps=5):
+    """One config sharded over the ranks (strong scaling): this rank's shard
+    of ONE instance, timed sets (max over ranks), plus one ShardComm.exchange
+    round (NCCL P2P halo) and one objective reduction (NCCL all-gather)."""
+    import numpy as np
+    import torch
+
+    from paper_2510_12897_b200 import _lib
+    from paper_2510_12897_b200.distributed import mpopf_comm, scopf_comm
+    from paper_2510_12897_b200.sharding import mpopf_shard
+    from paper_2510_12897_b200.synth import demand_curve, pglib_shaped
+    from paper_2510_12897_b200.workloads import build_workload, model_summary, n1_contingencies
+
+    dev = torch.device("cuda", local)
+    t_build = time.perf_counter()
+    head, base = name.split("_", 1)
+    comm = None
+    if head.startswith("n1"):
+        model = build_workload(name, lower_to_gpu=False, rank=rank, world=ws)
+        n_inst = len(n1_contingencies(pglib_shaped(base, seed=1), int(head[2:] or 1024))) + 1
+        if ws > 1:
+            comm = scopf_comm(model, n_inst, rank, ws)
+    else:
+        T = int(head[2:])
+        shard = mpopf_shard(pglib_shaped(base, seed=1), demand_curve(T), rank, ws, 0.25, lower_to_gpu=False)
+        model = shard.model
+        if ws > 1:
+            comm = mpopf_comm(shard, T, False, rank, ws)
+    summ = model_summary(model)
+    R = max(2, min(8, int(np.ceil(2 * L2_BYTES / summ["bytes_per_set"]))))
+    plans, bufs = replicas(model, R, local, seed0=500 + 10 * rank)
+    t_build = time.perf_counter() - t_build
+    lib = _lib.load()
+    stream = torch.cuda.Stream(dev)
+    launch = launcher(lib, plans, bufs, stream)
+    if ws > 1:
+        torch.distributed.barrier()
+    us = graph_us(launch, n_sets * R, stream, dev, reps=steps)
+    out = {"workload": name, "shard_bytes_per_set": summ["bytes_per_set"], "replicas": R, "build_s": t_build}
+    if comm is not None:
+        comm.setup()
+        xl = bufs[0]["x"].clone()
+        model.device_plan = plans[0]
+        for _ in range(3):
+            comm.exchange(xl)
+            comm.objective(xl)
+        torch.cuda.synchronize(dev)
+        torch.distributed.barrier()
+        n = 20
+        t0 = time.perf_counter()
+        for _ in range(n):
+            comm.exchange(xl)
+        torch.cuda.synchronize(dev)
+        t_ex = (time.perf_counter() - t0) / n
+        t0 = time.perf_counter()
+        for _ in range(n):
+            comm.objective(xl)
+        t_obj = (time.perf_counter() - t0) / n
+        t = torch.tensor([us, t_ex, t_obj], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        us, t_ex, t_obj = (float(v) for v in t.tolist())
+        out.update(halo_doubles=comm.halo_doubles(), exchange_us=1e6 * t_ex, objective_reduce_us=1e6 * t_obj,
+                   comm_note="wall time per call incl. host launch, max over ranks")
+    out.update(value=1e6 / us, unit="sets/s of the whole instance (every rank's shard per set)",
+               max_rank_us_per_set=us, n_ranks=ws)
+    del plans, bufs
+    torch.cuda.empty_cache()
+    return out
+
+
+def compressed_leg(model, plans, bufs, lib, stream, dev, peak):
+    """cons + compressed J/H values (exa_eval_set_compressed): the set kernel
+    into workspace scratch + one programmatic-dependent segmented-sum launch,
+    on the same rotating replicas; plus the host-buffer form end to end
+    (only c and the compressed values cross PCIe)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_2510_12897_b200 import model_patterns
+    from paper_2510_12897_b200.workloads import algorithmic_bytes
+
+    jp, hp = model_patterns(model)
+    R = len(plans)
+    hj = [jp.device_handle(p) for p in plans]
+    hh = [hp.device_handle(p) for p in plans]
+    for b in bufs:
+        b["Jc"] = torch.empty(jp.nnz, dtype=torch.float64, device=dev)
+        b["Hc"] = torch.empty(hp.nnz, dtype=torch.float64, device=dev)
+    sh = C.c_void_p(stream.cuda_stream)
+
+    def launch(i):
+        b, p = bufs[i % R], plans[i % R]
+        rc = lib.exa_eval_set_compressed(p.handle, None, hj[i % R], hh[i % R], b["x"].data_ptr(), b["y"].data_ptr(),
+                                         b["w"], b["c"].data_ptr(), b["Jc"].data_ptr(), b["Hc"].data_ptr(), sh)
+        if rc:
+            raise RuntimeError(lib.exa_last_error().decode())
+
+    us = graph_us(launch, 4 * R, stream, dev)
+    # bit-identical to sum_values of the raw slots (the reference's solver order)
+    with torch.cuda.stream(stream):
+        launch(0)
+        lib.exa_eval_set(plans[0].handle, None, bufs[0]["x"].data_ptr(), bufs[0]["y"].data_ptr(), bufs[0]["w"],
+                         bufs[0]["c"].data_ptr(), bufs[0]["J"].data_ptr(), bufs[0]["H"].data_ptr(), sh)
+    torch.cuda.synchronize(dev)
+    ok = bool(np.array_equal(hp.sum_values(bufs[0]["H"]).cpu().numpy().view(np.uint64),
+                             bufs[0]["Hc"].cpu().numpy().view(np.uint64)))
+    a = algorithmic_bytes(model)
+    cb = a["total"] - a["jac"] - a["hess"] + 8 * (jp.nnz + hp.nnz)
+    # host buffers, 3 streams in round robin (pinned), copies inside the timed region
+    NS = 3
+    slots = []
+    for k in range(NS):
+        wsp = C.c_void_p()
+        lib.exa_workspace_create(plans[0].handle, C.byref(wsp))
+        slots.append({"ws": wsp, "st": torch.cuda.Stream(dev),
+                      "x": bufs[0]["x"].cpu().pin_memory(), "y": bufs[0]["y"].cpu().pin_memory(),
+                      "c": torch.empty(model.ncon, dtype=torch.float64).pin_memory(),
+                      "Jc": torch.empty(jp.nnz, dtype=torch.float64).pin_memory(),
+                      "Hc": torch.empty(hp.nnz, dtype=torch.float64).pin_memory()})
+
+    def issue(i):
+        sl = slots[i % NS]
+        rc = lib.exa_eval_set_compressed_host(plans[0].handle, sl["ws"], hj[0], hh[0], sl["x"].data_ptr(),
+                                              sl["y"].data_ptr(), 1.0, sl["c"].data_ptr(), sl["Jc"].data_ptr(),
+                                              sl["Hc"].data_ptr(), C.c_void_p(sl["st"].cuda_stream))
+        if rc:
+            raise RuntimeError(lib.exa_last_error().decode())
+
+    for i in range(2 * NS):
+        issue(i)
+    for sl in slots:
+        sl["st"].synchronize()
+    n = 48
+    t0 = time.perf_counter()
+    for i in range(n):
+        issue(i)
+    for sl in slots:
+        sl["st"].synchronize()
+    e2e = n / (time.perf_counter() - t0)
+    for sl in slots:
+        lib.exa_workspace_destroy(sl["ws"])
+    return {"us_per_set": us, "value": 1e6 / us, "unit": "sets/s", "bytes_per_set": cb,
+            "frac": cb / us / 1e3 / peak, "nnz_jac": jp.nnz, "nnz_hess": hp.nnz,
+            "bit_equal_sum_values": ok,
+            "e2e": {"value": e2e, "unit": "sets/s", "h2d_bytes_per_step": 8 * (model.nvar + model.ncon),
+                    "d2h_bytes_per_step": 8 * (model.ncon + jp.nnz + hp.nnz),
+                    "path": "exa_eval_set_compressed_host, pinned buffers, 3 streams in round robin"},
+            "note": "bytes = x + y + parameters + c + compressed J and H (SURVEY 8d compressed variant); "
+                    "raw J/H live in workspace scratch (read back from L2 by the segmented sum)"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -236,12 +534,13 @@ def main():
     import torch
 
     from paper_2510_12897_b200 import _lib
-    from paper_2510_12897_b200.device import DevicePlan
-    from paper_2510_12897_b200.workloads import build_workload, eval_inputs, model_summary
+    from paper_2510_12897_b200.device import DevicePlan, host_layout
+    from paper_2510_12897_b200.workloads import (algorithmic_bytes_mode, build_workload, eval_inputs,
+                                                 model_summary)
 
     ws, rank, local = dist_setup()
     dev = torch.device("cuda", local)
-    sharded = args.workload.startswith(("mp", "n1", "scen"))
+    sharded = args.workload.startswith(SHARDED)
     # batched configs: this rank's shard of ONE instance (strong scaling);
     # single-instance configs: every rank evaluates its own sets (weak scaling)
     model = build_workload(args.workload, lower_to_gpu=False, rank=rank, world=ws if sharded else 1)
@@ -250,26 +549,11 @@ def main():
     R = max(2, int(np.ceil(2 * L2_BYTES / bps)))
     R = min(R, 64)
     lib = _lib.load()
-    plans, bufs = [], []
-    for r in range(R):
-        dp = DevicePlan(model, local)
-        x, y, w = eval_inputs(model, seed=1000 * rank + r)
-        bufs.append({
-            "x": torch.from_numpy(x).to(dev), "y": torch.from_numpy(y).to(dev), "w": w,
-            "c": torch.empty(model.ncon, dtype=torch.float64, device=dev),
-            "J": torch.empty(model.plan.n_jac_slots, dtype=torch.float64, device=dev),
-            "H": torch.empty(model.plan.n_hess_slots, dtype=torch.float64, device=dev),
-        })
-        plans.append(dp)
+    plans, bufs = replicas(model, R, local, seed0=1000 * rank)
     stream = torch.cuda.Stream(dev)
     sh = C.c_void_p(stream.cuda_stream)
-
-    def launch(i):
-        b = bufs[i % R]
-        rc = lib.exa_eval_set(plans[i % R].handle, None, b["x"].data_ptr(), b["y"].data_ptr(), b["w"],
-                              b["c"].data_ptr(), b["J"].data_ptr(), b["H"].data_ptr(), sh)
-        if rc:
-            raise RuntimeError(lib.exa_last_error().decode())
+    launch = launcher(lib, plans, bufs, stream)
+    exact_default = plans[0].exact_zero_sign
 
     S = args.sets_per_step
     # one CUDA graph = one step of S sets (rotating replicas); rotation phase kept across steps
@@ -296,14 +580,13 @@ def main():
             step(k)
     torch.cuda.synchronize(dev)
 
-    # parity spot check of replica 0 against the bitwise-equal numpy API path
-    ref_c = np.empty(model.ncon)
-    b0 = bufs[0]
+    # replica 0's outputs (point eval_inputs(model, 1000 * rank)): checked
+    # against the CPU oracle in the cpu_baseline leg
     with torch.cuda.stream(stream):
         launch(0)
     torch.cuda.synchronize(dev)
-    ref_c[:] = b0["c"].cpu().numpy()
-    assert np.isfinite(ref_c).all()
+    out0 = tuple(bufs[0][k].cpu().numpy() for k in ("c", "J", "H"))
+    assert all(np.isfinite(a).all() for a in out0)
 
     sampler = ClockSampler(local)
     with sampler:
@@ -349,11 +632,47 @@ def main():
     achieved = bps / per_launch_s / 1e9
     peak, peak_src = peaks()
     traffic, traffic_src = profiled_traffic(args.workload)
+    del graphs
+
+    extras = {}
+    if not args.no_extras and ws == 1 and not sharded:
+        # ---- isolated single-set latency (the set an IPM iteration waits for)
+        extras["latency"] = {"us_isolated": isolated_latency_us(launch, stream, dev),
+                             "us_pipelined": per_launch_s * 1e6,
+                             "note": "one set alone on the stream (no neighbour to overlap via PDL), "
+                                     "median of 35 CUDA-event intervals; us_pipelined = headline per-set time"}
+        # ---- the other zero-sign mode of the generated code, same rotation
+        alt_plans, alt_bufs = replicas(model, R, local, seed0=1000 * rank, exact_zero_sign=not exact_default)
+        us_alt = graph_us(launcher(lib, alt_plans, alt_bufs, stream), S * R if S * R <= 512 else S, stream, dev)
+        us_def = graph_us(launch, S * R if S * R <= 512 else S, stream, dev)
+        extras["zero_sign"] = {
+            "default": "exact" if exact_default else "relaxed",
+            "headline_mode_us_per_set": us_def,
+            "other_mode": "relaxed" if exact_default else "exact",
+            "other_mode_us_per_set": us_alt, "other_mode_value": 1e6 / us_alt,
+            "other_mode_frac": bps / us_alt / 1e3 / peak,
+            "note": "exact = the reference's bit patterns incl. signs of zero and NaN propagation of w * 0; "
+                    "relaxed = +0.0 structural zeros (IEEE-equal for finite multipliers)"}
+        del alt_plans, alt_bufs
+        # ---- separate callbacks (what an IPM calls each iteration), own bytes
+        cb = {}
+        for mode in ("cons", "jac", "hess", "obj", "grad"):
+            us = graph_us(launcher(lib, plans, bufs, stream, mode), 4 * R, stream, dev)
+            entry = {"us": us}
+            if mode in ("cons", "jac", "hess"):
+                mb = algorithmic_bytes_mode(model, mode)
+                entry.update(bytes=mb, GBps=mb / us / 1e3, frac=mb / us / 1e3 / peak)
+            cb[mode] = entry
+        cb["note"] = ("device time per call, graph of rotating replicas; obj = value kernel + pairwise leaves + "
+                      "combine, grad = gradient kernel + CSR reduce")
+        extras["callbacks"] = cb
+        # ---- compressed J/H (the values the reference solver consumes)
+        extras["compressed"] = compressed_leg(model, plans, bufs, lib, stream, dev, peak)
 
     # ---- extra (not the headline): NB independent sets per launch
     # (exa_eval_set_batch), for throughput on independent evaluation points
     batched = None
-    if not sharded and ws == 1 and info_batchable(plans[0]):
+    if not args.no_extras and not sharded and ws == 1 and info_batchable(plans[0]):
         NB = 8
         RB = max(2, int(np.ceil(2 * L2_BYTES / (NB * bps))))
         bb = []
@@ -372,27 +691,16 @@ def main():
             if rc:
                 raise RuntimeError(lib.exa_last_error().decode())
 
-        with torch.cuda.stream(stream):
-            for i in range(RB):
-                launch_b(i)
-            gb = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gb, stream=stream):
-                for i in range(4 * RB):
-                    launch_b(i)
-            gb.replay()
-        torch.cuda.synchronize(dev)
-        eb0, eb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            eb0.record(stream)
-            for _ in range(5):
-                gb.replay()
-            eb1.record(stream)
-        torch.cuda.synchronize(dev)
-        sb = 5 * 4 * RB * NB / (eb0.elapsed_time(eb1) / 1e3)
+        sb = 1e6 * NB / graph_us(launch_b, 4 * RB, stream, dev)
         batched = {"sets_per_launch": NB, "value": sb, "unit": "sets/s",
-                   "roofline_frac": sb * bps / 1e9 / peaks()[0],
+                   "roofline_frac": sb * bps / 1e9 / peak,
                    "note": "extra, not the headline: independent evaluation points per launch"}
         del bb
+
+    # ---- sharded configs over the ranks (multi-GPU readiness, strong scaling)
+    sharded_out = None
+    if not sharded and (ws > 1 or args.sharded_legs):
+        sharded_out = [sharded_leg(name, rank, ws, local) for name in ("mp96_case1354", "n1_case2000")]
 
     # ---- end to end: host buffers through the C ABI, copies inside the timed region.
     # exa_eval_set_host = H2D(x, y) + set kernel + D2H(c, J, H) on one stream;
@@ -462,6 +770,8 @@ def main():
         eval_callback_set(model, xp_, yp_, 1.0, cp_, Jp_, Hp_)
     e2e_numpy_pinned = n_np / (time.perf_counter() - t0)
     assert np.array_equal(Hp_, Hn) and np.array_equal(Jp_, Jn)
+    # the host path's H equals the device path's bit for bit (host-filled runs included)
+    assert np.array_equal(slots[0]["H"].numpy().view(np.uint64), slots[1]["H"].numpy().view(np.uint64))
     # latency view: one set at a time, synchronised per set
     t0 = time.perf_counter()
     for i in range(n_e2e // NS):
@@ -477,10 +787,11 @@ def main():
     e2e_value = n_e2e * (1 if sharded else ws) / e2e_dt
     h2d = 8 * (model.nvar + model.ncon)
     # D2H: c plus the x-dependent J/H ranges; the constant runs (constant J
-    # slots, structural-zero H pairs) are written into the host arrays by host
-    # threads inside the same call (plans[0].layout.fill_*)
+    # slots, structural-zero H pairs: +0.0 relaxed, weight * z exact) are
+    # written into the host arrays by host threads inside the same call
     lay0 = plans[0].layout
-    filled = 8 * int(lay0.fill_jac[:, 1].sum() + lay0.fill_hess[:, 1].sum())
+    filled = 8 * int(lay0.fill_jac[:, 1].sum() + (lay0.fill_hess[:, 1].sum() if len(lay0.fill_hess) else 0)
+                     + (lay0.fill_wzero[:, 1].sum() if len(lay0.fill_wzero) else 0))
     d2h = 8 * (model.ncon + model.plan.n_jac_slots + model.plan.n_hess_slots) - filled
 
     if rank != 0:
@@ -488,10 +799,10 @@ def main():
             torch.distributed.barrier()
             torch.distributed.destroy_process_group()
         return
-    cpu = None
+    cpu, parity = None, None
     if not args.no_cpu_baseline and bps < 2e9 and ws == 1:  # rank 0 at N=1 only
         xb, yb, wb = eval_inputs(model, 0)
-        cpu = cpu_baseline(model, xb, yb, wb, args.cpu_seconds, args.workload)
+        cpu, parity = cpu_baseline(model, xb, yb, wb, args.cpu_seconds, args.workload, gpu_out=out0)
     info = plans[0].info()
     line = {
         "metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": ws, "steps": args.steps,
@@ -503,7 +814,8 @@ def main():
             "hess_slots": summ["hess_slots"], "bytes_per_set": bps,
             "l2": f"rotating {R} full replicas ({R * bps / 2**20:.0f} MiB > 2x126 MiB L2)",
             "launch": "CUDA graph of single-set fused kernel launches (exa_k_set)",
-            "parallelism": (f"{'period' if args.workload.startswith('mp') else 'instance'} shards x{ws}"
+            "zero_sign": "exact" if exact_default else "relaxed",
+            "parallelism": (f"{'period' if args.workload.startswith(('mp', 'scen')) else 'instance'} shards x{ws}"
                             if sharded and ws > 1 else (f"replicas x{ws}" if ws > 1 else "single GPU")),
             "shard_bytes_per_set": bps,
         },
@@ -512,9 +824,10 @@ def main():
                      "kernel": "exa_k_set", "traffic_source": traffic_src,
                      "achieved_basis": "algorithmic bytes per set (SURVEY 8d) / mean per-launch time"},
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": {"value": e2e_value, "unit": "sets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": (f"exa_eval_set_host (C ABI): pinned host x,y -> HBM -> set kernel -> pinned host c,J,H; "
-                         f"one set per step, {NS} streams in round robin; constant J/H runs "
+                         f"one set per step, {NS} streams in round robin; constant / weighted-zero J/H runs "
                          f"({filled / 1e6:.1f} MB) written by host threads, not copied"),
                 "host_filled_bytes_per_step": filled,
                 "d2h_GBps": d2h * e2e_value / (1 if sharded else ws) / 1e9,
@@ -522,6 +835,8 @@ def main():
                 "numpy_api_pinned_value": e2e_numpy_pinned},
         "clocks": sampler.summary(),
         "batched": batched,
+        **extras,
+        "sharded": sharded_out,
         "gpu_launches": args.steps * S,
         "kernel_regs": info["regs_set_kernel"],
     }

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define EXA_ABI_VERSION 5
+#define EXA_ABI_VERSION 6
 #define EXA_MAXF 16
 #define EXA_MAXI 16
 #define EXA_MAXK 16
@@ -130,6 +130,18 @@ typedef struct ExaPlanDesc {
      instead of being copied from the device.  May be null / 0. */
   const int64_t* host_fill;
   int32_t n_fill_jac, n_fill_hess;
+  /* host path, exact zero-sign modules: raw H slot runs holding the
+     reference's weight * z (z = a structural +-0.0 of the pattern; the
+     weight is the row's multiplier or obj_weight), int64 quadruples (first
+     slot, length, offset into host_wzero_rows or -1 = obj_weight, IEEE-754
+     bits of z), sorted, disjoint from each other and from the host_fill H
+     runs.  Slot i of a run = mult_host[host_wzero_rows[offset + i]] * z,
+     computed by host threads from the caller's multipliers (sign of zero and
+     NaN / inf propagation as the reference's autodiff.py:652).  May be 0. */
+  const int64_t* host_wzero;
+  int32_t n_wzero, pad_wz;
+  const int32_t* host_wzero_rows;
+  int64_t n_wzero_rows;
 } ExaPlanDesc;
 
 /* ---- build-time: JIT ---------------------------------------------------- */
@@ -185,6 +197,32 @@ int exa_eval_cons_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, do
 int exa_eval_jac_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, double* jac_host, exa_stream_t stream);
 int exa_eval_hess_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, const double* mult_host,
                        double obj_weight, double* hess_host, exa_stream_t stream);
+/* ---- compressed values (what the reference solver consumes) ------------ */
+/* A compressed pattern on the plan's device (reference compress_coordinates /
+ * CompressedPattern, autodiff.py:660-689): nnz compressed entries over n_raw
+ * raw slots; entry k = 0 + sum of raw[ent[e]], e in [ptr[k], ptr[k+1]), in
+ * increasing e (np.bincount order, bit-identical to sum_values).  ptr: int64
+ * [nnz + 1] from 0 to n_raw; ent: int32 [n_raw] raw slot ids.  Host arrays,
+ * copied to the device. */
+typedef struct ExaPattern ExaPattern;
+int exa_pattern_create(ExaPlan* plan, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
+                       ExaPattern** out);
+void exa_pattern_destroy(ExaPattern* pattern);
+/* cons + COMPRESSED Jacobian and Hessian values of one point: the set kernel
+ * writes the raw slots into the workspace's scratch and the two segmented
+ * sums run in one programmatic-dependent launch behind it (reference
+ * solver._Scratch.jac / .hess = eval_* + sum_values, solver.py:282-295).
+ * jac_c has jpat's nnz entries, hess_c hpat's; a NULL pattern writes that
+ * output's raw slots instead.  Device pointers; asynchronous on `stream`. */
+int exa_eval_set_compressed(ExaPlan* plan, ExaWorkspace* ws, const ExaPattern* jpat, const ExaPattern* hpat,
+                            const double* x, const double* mult, double obj_weight, double* c, double* jac_c,
+                            double* hess_c, exa_stream_t stream);
+/* The same with HOST buffers: H2D x, mult; D2H c and the compressed values
+ * only (the raw slots never cross PCIe).  Pinned buffers: asynchronous on
+ * `stream`; pageable ones: complete on return. */
+int exa_eval_set_compressed_host(ExaPlan* plan, ExaWorkspace* ws, const ExaPattern* jpat, const ExaPattern* hpat,
+                                 const double* x_host, const double* mult_host, double obj_weight, double* c_host,
+                                 double* jac_c_host, double* hess_c_host, exa_stream_t stream);
 /* out[k] = 0 + sum_{e in [ptr[k], ptr[k+1])} raw[ent[e]], sequentially in e
  * order (np.bincount order); with ent sorted by raw slot within each k this is
  * CompressedPattern.sum_values.  All pointers are device pointers. */

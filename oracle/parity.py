@@ -35,10 +35,15 @@ def ieee_equal(a, b) -> bool:
 
 
 def bit_equal(a, b) -> bool:
-    """Identical IEEE-754 bit patterns (signs of zero included)."""
+    """Identical IEEE-754 bit patterns (signs of zero included); NaNs match
+    any NaN (IEEE leaves the payload unspecified: x86 and the GPU produce
+    different default NaNs)."""
     a = np.ascontiguousarray(a, dtype=np.float64)
     b = np.ascontiguousarray(b, dtype=np.float64)
-    return a.shape == b.shape and bool(np.array_equal(a.view(np.uint64), b.view(np.uint64)))
+    if a.shape != b.shape:
+        return False
+    same = a.view(np.uint64) == b.view(np.uint64)
+    return bool(np.all(same | (np.isnan(a) & np.isnan(b))))
 
 
 def strict_mask(gpu, ref, rtol=RTOL):

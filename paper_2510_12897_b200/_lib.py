@@ -16,7 +16,7 @@ MAXF = MAXI = MAXK = 16
 NMODES = 6
 NKERN = 12
 MODE_SET, MODE_CONS, MODE_JAC, MODE_HESS, MODE_OBJV, MODE_GRAD = range(6)
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 i64, i32, dbl, vp = C.c_int64, C.c_int32, C.c_double, C.c_void_p
 
@@ -50,6 +50,8 @@ class PlanDesc(C.Structure):
         ("cubin", vp), ("cubin_size", i64),
         ("has_domain_checks", i32),
         ("persist", i32 * NKERN), ("pdl", i32), ("batchable", i32), ("host_fill", C.POINTER(C.c_int64)), ("n_fill_jac", i32), ("n_fill_hess", i32),
+        ("host_wzero", C.POINTER(C.c_int64)), ("n_wzero", i32), ("pad_wz", i32),
+        ("host_wzero_rows", C.POINTER(C.c_int32)), ("n_wzero_rows", i64),
     ]
 
 
@@ -76,6 +78,10 @@ SIGNATURES = {
     "exa_eval_hess_host": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp]),
     "exa_eval_set_batch": (C.c_int, [vp, vp, i64, vp, vp, dbl, vp, vp, vp, vp]),
     "exa_segment_sum": (C.c_int, [i64, vp, vp, vp, vp, vp]),
+    "exa_pattern_create": (C.c_int, [vp, i64, i64, vp, vp, C.POINTER(vp)]),
+    "exa_pattern_destroy": (None, [vp]),
+    "exa_eval_set_compressed": (C.c_int, [vp, vp, vp, vp, vp, vp, dbl, vp, vp, vp, vp]),
+    "exa_eval_set_compressed_host": (C.c_int, [vp, vp, vp, vp, vp, vp, dbl, vp, vp, vp, vp]),
     "exa_kkt_values": (C.c_int, [i64, vp, vp, vp, vp, dbl, dbl, vp, vp]),
     "exa_domain_error": (C.c_int, [vp, vp, vp, C.POINTER(i64), C.POINTER(i32), C.POINTER(i64)]),
     "exa_last_error": (C.c_char_p, []),

@@ -384,6 +384,29 @@ class CompressedPattern:
         self._dev_csr = cache
         return cache
 
+    def device_handle(self, dp):
+        """The pattern as an ``ExaPattern`` on ``dp``'s device (created once)."""
+        handles = self.__dict__.setdefault("_exa_handles", {})
+        h = handles.get(dp.device)
+        if h is None:
+            order = np.argsort(self.slot_map, kind="stable")
+            ptr = np.zeros(self.nnz + 1, dtype=np.int64)
+            np.cumsum(np.bincount(self.slot_map, minlength=self.nnz), out=ptr[1:])
+            ent = np.ascontiguousarray(order.astype(np.int32))
+            h = C.c_void_p()
+            _lib.check(dp._lib.exa_pattern_create(dp.handle, int(self.slot_map.size), self.nnz,
+                                                  ptr.ctypes.data, ent.ctypes.data, C.byref(h)),
+                       "exa_pattern_create")
+            handles[dp.device] = h
+        return h
+
+    def __del__(self):
+        for h in getattr(self, "_exa_handles", {}).values():
+            try:
+                _lib.load().exa_pattern_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+
     def sum_values(self, raw_values):
         torch = _torch()
         if not torch.cuda.is_available():
@@ -415,3 +438,47 @@ def compress_coordinates(rows, cols) -> CompressedPattern:
     uniq, inverse = np.unique(np.stack([rows, cols], axis=1), axis=0, return_inverse=True)
     return CompressedPattern(uniq[:, 0].astype(np.int64), uniq[:, 1].astype(np.int64),
                              inverse.astype(np.int64).ravel())
+
+
+def model_patterns(model):
+    """(Jacobian, Hessian) CompressedPattern of a model, built once (host
+    sparsity work, reference ``solver._Scratch.__init__``, solver.py:252-262)."""
+    pats = getattr(model, "_exa_patterns", None)
+    if pats is None:
+        pats = (compress_coordinates(*jacobian_structure(model)), compress_coordinates(*hessian_structure(model)))
+        model._exa_patterns = pats
+    return pats
+
+
+def eval_callback_set_compressed(model, x, mult, obj_weight: float, out_c, out_jac, out_hess) -> None:
+    """cons + COMPRESSED Jacobian / Hessian values at one point -- what the
+    reference solver consumes every iteration (``solver.py:282-295``:
+    ``eval_jacobian`` / ``eval_hessian`` followed by ``sum_values``).
+
+    ``out_jac`` / ``out_hess`` have ``model_patterns(model)[i].nnz`` entries,
+    bit-identical to ``pattern.sum_values(raw)``.  One set kernel writes the raw
+    slots into device scratch and one segmented-sum launch compresses them; for
+    numpy buffers only c and the compressed values cross PCIe."""
+    x = _check_x(model, x)
+    mult = _check_mult(model, mult)
+    jp, hp = model_patterns(model)
+    for buf, n, what in ((out_c, model.ncon, "constraint"), (out_jac, jp.nnz, "compressed jacobian"),
+                         (out_hess, hp.nnz, "compressed hessian")):
+        if _shape(buf) != (n,):
+            raise ValueError(f"{what} buffer has shape {_shape(buf)}, expected ({n},)")
+    dp = _dplan(model)
+    jh, hh = jp.device_handle(dp), hp.device_handle(dp)
+    if not _is_cuda(x) and not _is_cuda(mult) and _host_outputs(out_c, out_jac, out_hess):
+        return _host_call(dp, "exa_eval_set_compressed_host", "set", jh, hh, x, mult, float(obj_weight),
+                          out_c, out_jac, out_hess)
+    st = _Stage(dp)
+    xp = st.inp(x)
+    yp = st.inp(mult) if model.ncon else 0
+    cp = st.out(out_c, model.ncon)
+    jcp = st.out(out_jac, jp.nnz)
+    hcp = st.out(out_hess, hp.nnz)
+    s = st.stream()
+    _lib.check(dp._lib.exa_eval_set_compressed(dp.handle, dp.workspace(), jh, hh, xp, yp, float(obj_weight), cp, jcp,
+                                               hcp, s), "eval_set_compressed")
+    _raise_domain(dp, s, "set")
+    st.finish()

@@ -47,10 +47,12 @@ def _zero_const(v) -> bool:
     return float(v.value if isinstance(v, Arr) else v) == 0.0
 
 
-# EXA_EXACT_ZERO_SIGN=1 keeps every 0 + x of the reference and the sign of the
-# structural zeros w * 0 (bitwise identical signs of zero in J/H); the default
-# drops the former in derivative space (see Gen.bin) and writes the latter as
-# +0.0 without loading the weight -- IEEE-equal values either way
+# Zero-sign mode of the generated code.  Exact: every 0 + x of the reference
+# and the structural zeros w * 0 with their weight's sign (bit-identical J/H,
+# NaN / inf multipliers propagate like the reference's).  Relaxed: the former
+# dropped in derivative space (see Gen.bin), the latter written as +0.0
+# without loading the weight -- IEEE-equal for finite weights.  The default is
+# EXA_EXACT_ZERO_SIGN (1 = exact); a layout may choose per plan (relax=...).
 _DERIV_ZERO_ELISION = os.environ.get("EXA_EXACT_ZERO_SIGN", "0") != "1"
 # term-group members' multipliers (their own rows: each read once per set) are
 # loaded evict-first like the parameters (case13659 6.08 -> 5.99 us, MP96 39.4
@@ -283,8 +285,9 @@ class Gen:
 class PatternCode:
     """Generated source for one tape pattern plus what it needs at run time."""
 
-    def __init__(self, pid: int, tape, field_count: int, index_count: int, slot_struct):
+    def __init__(self, pid: int, tape, field_count: int, index_count: int, slot_struct, relax: bool | None = None):
         self.pid = pid
+        self.relax = _DERIV_ZERO_ELISION if relax is None else bool(relax)
         self.tape = tape
         self.nf = field_count
         self.ni = index_count
@@ -561,7 +564,7 @@ class PatternCode:
         n_value_lines = len(g.lines)
 
         # first order
-        g.deriv = _DERIV_ZERO_ELISION
+        g.deriv = self.relax
         adj = self._adjoints(g, v) if k else None
         grads = self._slot_sums(g, adj) if k else []
         n_grad_lines = len(g.lines)
@@ -578,14 +581,19 @@ class PatternCode:
         # caller's arrays instead of copying them over PCIe (exa_eval_set_host).
         self.jconst = {s: float(grads[s].value if isinstance(grads[s], Arr) else grads[s])
                        for s in range(k) if not isinstance(grads[s], Sym)}
-        self.hzero = []
-        if _DERIV_ZERO_ELISION:
-            pair = 0
-            for i in range(k):
-                for j in range(i + 1):
-                    if _zero_const(by_seed[j][i]):
-                        self.hzero.append(pair)
-                    pair += 1
+        # structural-zero Hessian pairs: (pair, the constant z) -- the slot's
+        # value is weight * z, +0.0 under the relaxation (self.hzero); in the
+        # exact mode the host path computes weight * z from the caller's
+        # multipliers (self.hzero_w)
+        self.hzero, self.hzero_w = [], []
+        pair = 0
+        for i in range(k):
+            for j in range(i + 1):
+                val = by_seed[j][i]
+                if _zero_const(val):
+                    (self.hzero if self.relax else self.hzero_w).append(
+                        pair if self.relax else (pair, float(val.value if isinstance(val, Arr) else val)))
+                pair += 1
 
         out = []
         pid = self.pid
@@ -641,7 +649,7 @@ class PatternCode:
                     bi, bj = self.slot_struct[i][0], self.slot_struct[j][0]
                     if i != j and bi == bj:
                         expr = f"(c{i} == c{j} ? {expr} * 2.0 : {expr})"
-                    if _DERIV_ZERO_ELISION and _zero_const(val):
+                    if self.relax and _zero_const(val):
                         out.append(f"      Hout[T.hess0 + {pair}LL * T.nrec + o] = 0.0;  // structural zero")
                     else:
                         out.append(f"      Hout[T.hess0 + {pair}LL * T.nrec + o] = wgt * {expr};")
@@ -663,7 +671,7 @@ class PatternCode:
             # augment's J/H slots from the row thread), same replay as above
             gx = Gen()
             vx = self._values(gx, {"field": {}, "var": [Sym("x0")]})
-            gx.deriv = _DERIV_ZERO_ELISION
+            gx.deriv = self.relax
             adjx = self._adjoints(gx, vx)
             gradx = self._slot_sums(gx, adjx)
             tx = self._tangents(gx, vx, 0)
@@ -677,7 +685,7 @@ class PatternCode:
             out.append(f"__device__ __forceinline__ void exa_termx_{pid}(const double x0, const double wgt, double& jv, double& hv) {{")
             out.extend(gx.lines)
             out.append(f"  jv = {R(gradx[0])};")
-            out.append("  hv = 0.0;" if (_DERIV_ZERO_ELISION and _zero_const(colx[0])) else f"  hv = wgt * {R(colx[0])};")
+            out.append("  hv = 0.0;" if (self.relax and _zero_const(colx[0])) else f"  hv = wgt * {R(colx[0])};")
             out.append("}")
         # records per thread: light patterns amortise per-thread overheads and
         # overlap several records' loads; heavy ones keep one record per thread
@@ -690,13 +698,13 @@ class PatternCode:
 
     def group_source(self, gid: int, members: list) -> str:
         """Group of terms of this one pattern (see :func:`group_source`)."""
-        return group_source(gid, [(self, mem) for mem in members])
+        return group_source(gid, [(self, mem) for mem in members], relax=self.relax)
 
     def tape_norm(self):
         return list(self.tape.instr)
 
 
-def group_source(gid: int, entries: list, augs: list = ()) -> str:
+def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = None) -> str:
     """One thread evaluates record r of several terms (a *term group*).
 
     ``entries[m] = (PatternCode, {"cols": [group column id per index column],
@@ -713,6 +721,7 @@ def group_source(gid: int, entries: list, augs: list = ()) -> str:
     ``off + r`` (single-variable, field-free pattern gathering the same
     variable as the member's slot), weighted by the multiplier of the row the
     augment record adds into."""
+    relax = _DERIV_ZERO_ELISION if relax is None else bool(relax)
     M = len(entries)
     g = Gen()
     pre, post = [], []
@@ -773,7 +782,7 @@ def group_source(gid: int, entries: list, augs: list = ()) -> str:
         g.lines.append(f"  if ((MODE & EXA_M_OBJV) && {T}.kind == EXA_OBJ) A.V[{T}.scr0 + r] = {R(root)};")
         if not k:
             continue
-        g.deriv = _DERIV_ZERO_ELISION
+        g.deriv = relax
         adj = pc._adjoints(g, v)
         grads = pc._slot_sums(g, adj)
         for s_ in range(k):
@@ -790,7 +799,7 @@ def group_source(gid: int, entries: list, augs: list = ()) -> str:
                 if dup:
                     expr = f"({cnames[m][i]} == {cnames[m][j]} ? {expr} * 2.0 : {expr})"
                 pair = i * (i + 1) // 2 + j
-                if _DERIV_ZERO_ELISION and _zero_const(col[i]):  # structural zero: +0.0, no weight
+                if relax and _zero_const(col[i]):  # structural zero: +0.0, no weight
                     early.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = 0.0;")
                     continue
                 dst = early if (const(col[i]) and not dup) else g.lines
@@ -799,7 +808,7 @@ def group_source(gid: int, entries: list, augs: list = ()) -> str:
     aug_late = []
     for k, (apc, off, m, s_) in enumerate(augs):
         xs = vsyms[m][s_].name
-        if _DERIV_ZERO_ELISION and getattr(apc, "termx_hzero", False):
+        if relax and getattr(apc, "termx_hzero", False):
             # structural-zero Hessian entry: written as +0.0 (the reference's
             # w * 0.0 carries the multiplier's sign; IEEE-equal, see the zero-sign
             # relaxation) -- saves a two-load chain per record

@@ -17,6 +17,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <condition_variable>
@@ -79,8 +80,12 @@ struct ExaWorkspace {
   unsigned long long* err = nullptr;
   cudaStream_t aux = nullptr;   // second stream: light kernel runs beside the heavy one
   cudaEvent_t fork = nullptr, join = nullptr;
-  /* device staging for exa_eval_set_host (allocated on first use) */
+  /* device staging for exa_eval_set_host (allocated on first use); dJ / dH
+     are also the raw-slot scratch of exa_eval_set_compressed */
   double *dx = nullptr, *dy = nullptr, *dc = nullptr, *dJ = nullptr, *dH = nullptr;
+  /* compressed J / H staging of exa_eval_set_compressed_host */
+  double *dJc = nullptr, *dHc = nullptr;
+  int64_t cap_Jc = 0, cap_Hc = 0;
   /* pinned host staging for pageable callers: x, mult | c, J ranges, H ranges */
   double* hstage = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
@@ -121,8 +126,23 @@ struct ExaPlan {
   /* host path: constant runs filled on the host, (first, length, value) */
   struct Run { int64_t a, n; double v; };
   std::vector<Run> fill_jac, fill_hess;
+  /* ... and weighted-zero runs (exact zero-sign modules): slot a + i holds
+     mult[rows[off + i]] * z (off < 0: obj_weight * z) */
+  struct WRun { int64_t a, n, off; double z; };
+  std::vector<WRun> fill_wz;
+  std::vector<int32_t> wz_rows;
   /* ... and the complementary slot ranges copied D2H, (first, length) */
   std::vector<std::pair<int64_t, int64_t>> copy_jac, copy_hess;
+};
+
+/* A compressed pattern (reference CompressedPattern, autodiff.py:660-674) on
+ * the plan's device: compressed entry k sums raw slots ent[ptr[k] .. ptr[k+1])
+ * in increasing slot order (np.bincount order). */
+struct ExaPattern {
+  int device = 0;
+  int64_t n_raw = 0, nnz = 0;
+  int64_t* ptr = nullptr;
+  int32_t* ent = nullptr;
 };
 
 // ---------------------------------------------------------------------------
@@ -241,6 +261,33 @@ __global__ void exa_compress_reduce(int64_t nnz, const int64_t* __restrict__ ptr
   const int64_t e1 = ptr[k + 1];
   for (int64_t e = ptr[k]; e < e1; ++e) acc = acc + __ldg(raw + __ldg(ent + e));
   out[k] = acc;
+}
+
+// Compressed J and H of one callback set in one launch (entries [0, nJ) are
+// J's, the rest H's).  Launched as a programmatic dependent of the set
+// kernel: the CTAs load their CSR ranges, then wait for the set's raw slots.
+__global__ void __launch_bounds__(256) exa_compress2_kernel(
+    int64_t nJ, const int64_t* __restrict__ ptrJ, const int32_t* __restrict__ entJ, const double* rawJ,
+    double* __restrict__ outJ, int64_t nH, const int64_t* __restrict__ ptrH, const int32_t* __restrict__ entH,
+    const double* rawH, double* __restrict__ outH) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool isJ = i < nJ;
+  const int64_t k = isJ ? i : i - nJ;
+  const bool live = isJ || k < nH;
+  const int64_t* ptr = isJ ? ptrJ : ptrH;
+  const int32_t* ent = isJ ? entJ : entH;
+  int64_t e0 = 0, e1 = 0;
+  if (live) {
+    e0 = __ldg(ptr + k);
+    e1 = __ldg(ptr + k + 1);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!live) return;
+  const double* raw = isJ ? rawJ : rawH;
+  double acc = 0.0;
+  for (int64_t e = e0; e < e1; ++e) acc = acc + raw[__ldg(ent + e)];  // plain load: written by the set
+  (isJ ? outJ : outH)[k] = acc;
 }
 
 // KKT assembly (reference solver.py:421-456): one thread per lower-triangle
@@ -385,6 +432,8 @@ void exa_workspace_destroy(ExaWorkspace* w) {
   cudaFree(w->dc);
   cudaFree(w->dJ);
   cudaFree(w->dH);
+  cudaFree(w->dJc);
+  cudaFree(w->dHc);
   if (w->hstage) cudaFreeHost(w->hstage);
   for (cudaEvent_t e : w->chunk_ev) cudaEventDestroy(e);
   if (w->fork) cudaEventDestroy(w->fork);
@@ -443,25 +492,53 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
   }
   p->batchable = d->batchable && !d->has_domain_checks;
   {
+    // host-filled runs; the complement of each output's runs is copied D2H
     auto take = [&](const int64_t* tr, int n, int64_t total, std::vector<ExaPlan::Run>& fill,
-                    std::vector<std::pair<int64_t, int64_t>>& copy) -> int {
-      int64_t at = 0;
+                    std::vector<std::pair<int64_t, int64_t>>* spans) -> int {
       for (int i = 0; i < n; ++i) {
         const int64_t a = tr[3 * i], len = tr[3 * i + 1];
         double v;
         std::memcpy(&v, &tr[3 * i + 2], sizeof v);
-        if (a < at || len <= 0 || a + len > total) return fail("host_fill: runs must be sorted, disjoint, in range");
-        if (a > at) copy.push_back({at, a - at});
+        if (len <= 0 || a < 0 || a + len > total) return fail("host_fill: run out of range");
         fill.push_back({a, len, v});
-        at = a + len;
+        spans->push_back({a, len});
+      }
+      return 0;
+    };
+    auto complement = [&](std::vector<std::pair<int64_t, int64_t>>& spans, int64_t total,
+                          std::vector<std::pair<int64_t, int64_t>>& copy) -> int {
+      std::sort(spans.begin(), spans.end());
+      int64_t at = 0;
+      for (auto& sp : spans) {
+        if (sp.first < at) return fail("host_fill: runs must be disjoint");
+        if (sp.first > at) copy.push_back({at, sp.first - at});
+        at = sp.first + sp.second;
       }
       if (at < total) copy.push_back({at, total - at});
       return 0;
     };
     const int nj = d->host_fill ? d->n_fill_jac : 0, nh = d->host_fill ? d->n_fill_hess : 0;
-    if ((rc = take(d->host_fill, nj, d->n_jac, p->fill_jac, p->copy_jac))) return bail(rc);
-    if ((rc = take(d->host_fill ? d->host_fill + 3 * nj : nullptr, nh, d->n_hess, p->fill_hess, p->copy_hess)))
+    std::vector<std::pair<int64_t, int64_t>> sj, sh;
+    if ((rc = take(d->host_fill, nj, d->n_jac, p->fill_jac, &sj))) return bail(rc);
+    if ((rc = take(d->host_fill ? d->host_fill + 3 * nj : nullptr, nh, d->n_hess, p->fill_hess, &sh)))
       return bail(rc);
+    const int nw = d->host_wzero ? d->n_wzero : 0;
+    for (int i = 0; i < nw; ++i) {
+      const int64_t* q = d->host_wzero + 4 * i;
+      double z;
+      std::memcpy(&z, &q[3], sizeof z);
+      if (q[1] <= 0 || q[0] < 0 || q[0] + q[1] > d->n_hess || (q[2] >= 0 && q[2] + q[1] > d->n_wzero_rows))
+        return bail(fail("host_wzero: run out of range"));
+      p->fill_wz.push_back({q[0], q[1], q[2], z});
+      sh.push_back({q[0], q[1]});
+    }
+    if (d->n_wzero_rows > 0) {
+      p->wz_rows.assign(d->host_wzero_rows, d->host_wzero_rows + d->n_wzero_rows);
+      for (int32_t r : p->wz_rows)
+        if (r < 0 || r >= d->ncon) return bail(fail("host_wzero_rows: row out of range"));
+    }
+    if ((rc = complement(sj, d->n_jac, p->copy_jac))) return bail(rc);
+    if ((rc = complement(sh, d->n_hess, p->copy_hess))) return bail(rc);
   }
   p->threads[0] = d->threads[0] > 0 ? d->threads[0] : 128;
   p->threads[1] = d->threads[1] > 0 ? d->threads[1] : 256;
@@ -697,7 +774,10 @@ int exa_eval_set_batch(ExaPlan* p, ExaWorkspace* ws, int64_t nsets, const double
 namespace {
 struct FillPool {
   // dst[0, n) = v, or (src) = src[0, n) once event ev (if any) has completed
-  struct Piece { double* dst; int64_t n; double v; const double* src = nullptr; cudaEvent_t ev = nullptr; };
+  struct Piece {
+    double* dst; int64_t n; double v; const double* src = nullptr; cudaEvent_t ev = nullptr;
+    const int32_t* rows = nullptr; const double* mult = nullptr;  // weighted zeros: dst[i] = mult[rows[i]] * v
+  };
   std::mutex call_mu;  // one fill at a time
   std::mutex mu;
   std::condition_variable cv;
@@ -708,7 +788,9 @@ struct FillPool {
   std::atomic<int> active{0};
 
   static void run(const Piece& q) {
-    if (q.src) {
+    if (q.rows) {
+      for (int64_t i = 0; i < q.n; ++i) q.dst[i] = q.mult[q.rows[i]] * q.v;
+    } else if (q.src) {
       if (q.ev) cudaEventSynchronize(q.ev);
       std::memcpy(q.dst, q.src, q.n * sizeof(double));
     } else if (q.v == 0.0 && !std::signbit(q.v)) {
@@ -777,13 +859,27 @@ FillPool& fill_pool() {
 
 constexpr int64_t kPiece = 32768;  // doubles (256 KB) per host-pool piece
 
-static void add_fill(const ExaPlan* p, double* jac, double* hess, std::vector<FillPool::Piece>& pcs) {
+static void add_fill(const ExaPlan* p, double* jac, double* hess, const double* mult, double w_obj,
+                     std::vector<FillPool::Piece>& pcs) {
   for (auto* rs : {&p->fill_jac, &p->fill_hess}) {
     double* out = rs == &p->fill_jac ? jac : hess;
     if (!out) continue;
     for (auto& r : *rs)
       for (int64_t o = 0; o < r.n; o += kPiece) pcs.push_back({out + r.a + o, r.n - o < kPiece ? r.n - o : kPiece, r.v});
   }
+  if (!hess) return;
+  for (auto& r : p->fill_wz)
+    for (int64_t o = 0; o < r.n; o += kPiece) {
+      const int64_t n = r.n - o < kPiece ? r.n - o : kPiece;
+      if (r.off < 0) {  // objective weight: a constant run
+        pcs.push_back({hess + r.a + o, n, w_obj * r.z});
+      } else {
+        FillPool::Piece q{hess + r.a + o, n, r.z};
+        q.rows = p->wz_rows.data() + r.off + o;
+        q.mult = mult;
+        pcs.push_back(q);
+      }
+    }
 }
 
 static bool pageable(const void* ptr) {
@@ -808,6 +904,18 @@ static std::vector<Range> d2h_ranges(const ExaPlan* p, const ExaWorkspace* w, do
   return r;
 }
 
+// Device staging of a workspace, sized for its plan (first use; caller holds w->mu).
+static int ws_staging(ExaPlan* p, ExaWorkspace* w) {
+  if (w->dx) return 0;
+  CU(cudaSetDevice(p->device));
+  CU(cudaMalloc((void**)&w->dx, (p->nvar > 0 ? p->nvar : 1) * sizeof(double)));
+  CU(cudaMalloc((void**)&w->dy, (p->ncon > 0 ? p->ncon : 1) * sizeof(double)));
+  CU(cudaMalloc((void**)&w->dc, (p->ncon > 0 ? p->ncon : 1) * sizeof(double)));
+  CU(cudaMalloc((void**)&w->dJ, (p->n_jac > 0 ? p->n_jac : 1) * sizeof(double)));
+  CU(cudaMalloc((void**)&w->dH, (p->n_hess > 0 ? p->n_hess : 1) * sizeof(double)));
+  return 0;
+}
+
 // Host-buffer form of one callback (mode SET, CONS, JAC or HESS): H2D of the
 // inputs the mode reads, the device callback on the workspace's staging, D2H
 // of its x-dependent output ranges, constant runs filled on the host.  Null
@@ -818,14 +926,7 @@ static int host_eval(ExaPlan* p, ExaWorkspace* ws, int mode, const double* x, co
   DeviceGuard dguard(p->device);
   ExaWorkspace* w = ws ? ws : p->dflt;
   std::unique_lock<std::mutex> lazy(w->mu);
-  if (!w->dx) {  // first use: device staging sized for this plan
-    CU(cudaSetDevice(p->device));
-    CU(cudaMalloc((void**)&w->dx, (p->nvar > 0 ? p->nvar : 1) * sizeof(double)));
-    CU(cudaMalloc((void**)&w->dy, (p->ncon > 0 ? p->ncon : 1) * sizeof(double)));
-    CU(cudaMalloc((void**)&w->dc, (p->ncon > 0 ? p->ncon : 1) * sizeof(double)));
-    CU(cudaMalloc((void**)&w->dJ, (p->n_jac > 0 ? p->n_jac : 1) * sizeof(double)));
-    CU(cudaMalloc((void**)&w->dH, (p->n_hess > 0 ? p->n_hess : 1) * sizeof(double)));
-  }
+  if (int rc_ = ws_staging(p, w)) return rc_;
   if (mode != EXA_MODE_SET && mode != EXA_MODE_HESS) mult = nullptr;
   if (mode != EXA_MODE_SET && mode != EXA_MODE_CONS) c = nullptr;
   if (mode != EXA_MODE_SET && mode != EXA_MODE_JAC) jac = nullptr;
@@ -910,7 +1011,7 @@ static int host_eval(ExaPlan* p, ExaWorkspace* ws, int mode, const double* x, co
       }
     }
   }
-  add_fill(p, jac, hess, pcs);
+  add_fill(p, jac, hess, mult, w_obj, pcs);
   if (!pcs.empty()) fill_pool().fill(pcs);
   return 0;
 }
@@ -931,6 +1032,122 @@ int exa_eval_jac_host(ExaPlan* p, ExaWorkspace* ws, const double* x, double* jac
 int exa_eval_hess_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj,
                        double* hess, exa_stream_t stream) {
   return host_eval(p, ws, EXA_MODE_HESS, x, mult, w_obj, nullptr, nullptr, hess, (cudaStream_t)stream);
+}
+
+int exa_pattern_create(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
+                       ExaPattern** out) {
+  if (!p || !out || n_raw < 0 || nnz < 0 || (nnz && !ptr) || (n_raw && !ent))
+    return fail("exa_pattern_create: invalid argument");
+  *out = nullptr;
+  if (ptr && (ptr[0] != 0 || ptr[nnz] != n_raw)) return fail("exa_pattern_create: ptr must run from 0 to n_raw");
+  for (int64_t k = 0; k < nnz; ++k)
+    if (ptr[k + 1] < ptr[k]) return fail("exa_pattern_create: ptr must be non-decreasing");
+  for (int64_t e = 0; e < n_raw; ++e)
+    if (ent[e] < 0 || ent[e] >= n_raw) return fail("exa_pattern_create: raw slot %lld out of range", (long long)e);
+  DeviceGuard g(p->device);
+  ExaPattern* q = new ExaPattern();
+  q->device = p->device;
+  q->n_raw = n_raw;
+  q->nnz = nnz;
+  int rc = dev_upload(&q->ptr, ptr, (size_t)(nnz + 1));
+  if (!rc) rc = dev_upload(&q->ent, ent, (size_t)n_raw);
+  if (rc) {
+    exa_pattern_destroy(q);
+    return rc;
+  }
+  *out = q;
+  return 0;
+}
+
+void exa_pattern_destroy(ExaPattern* q) {
+  if (!q) return;
+  cudaFree(q->ptr);
+  cudaFree(q->ent);
+  delete q;
+}
+
+// raw J / H of the set into the workspace scratch, then both segmented sums in
+// one programmatic-dependent launch (a NULL pattern: that output gets the raw
+// slots themselves)
+static int set_compressed(ExaPlan* p, ExaWorkspace* w, const ExaPattern* jp, const ExaPattern* hp, const double* x,
+                          const double* mult, double w_obj, double* c, double* jc, double* hc, cudaStream_t st) {
+  if ((jp && jp->n_raw != p->n_jac) || (hp && hp->n_raw != p->n_hess))
+    return fail("exa_eval_set_compressed: pattern does not match the plan's raw J / H slots");
+  if ((jp && jp->device != p->device) || (hp && hp->device != p->device))
+    return fail("exa_eval_set_compressed: pattern on another device");
+  double* rawJ = jp ? w->dJ : jc;
+  double* rawH = hp ? w->dH : hc;
+  int rc = exa_eval_set(p, w, x, mult, w_obj, c, rawJ, rawH, st);
+  if (rc) return rc;
+  const int64_t nJ = jp ? jp->nnz : 0, nH = hp ? hp->nnz : 0;
+  if (nJ + nH == 0) return 0;
+  const int64_t* ptrJ = jp ? jp->ptr : nullptr;
+  const int32_t* entJ = jp ? jp->ent : nullptr;
+  const int64_t* ptrH = hp ? hp->ptr : nullptr;
+  const int32_t* entH = hp ? hp->ent : nullptr;
+  const double* cJ = rawJ;
+  const double* cH = rawH;
+  void* args[] = {(void*)&nJ, (void*)&ptrJ, (void*)&entJ, (void*)&cJ, (void*)&jc,
+                  (void*)&nH, (void*)&ptrH, (void*)&entH, (void*)&cH, (void*)&hc};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid_for(nJ + nH, 256));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = p->pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CU(cudaLaunchKernelExC(&cfg, (const void*)exa_compress2_kernel, args));
+  return 0;
+}
+
+int exa_eval_set_compressed(ExaPlan* p, ExaWorkspace* ws, const ExaPattern* jpat, const ExaPattern* hpat,
+                            const double* x, const double* mult, double w_obj, double* c, double* jac_c,
+                            double* hess_c, exa_stream_t stream) {
+  if (!p) return fail("null plan");
+  DeviceGuard dguard(p->device);
+  ExaWorkspace* w = ws ? ws : p->dflt;
+  {
+    std::lock_guard<std::mutex> lazy(w->mu);
+    if (int rc_ = ws_staging(p, w)) return rc_;
+  }
+  return set_compressed(p, w, jpat, hpat, x, mult, w_obj, c, jac_c, hess_c, (cudaStream_t)stream);
+}
+
+int exa_eval_set_compressed_host(ExaPlan* p, ExaWorkspace* ws, const ExaPattern* jpat, const ExaPattern* hpat,
+                                 const double* x, const double* mult, double w_obj, double* c, double* jac_c,
+                                 double* hess_c, exa_stream_t stream) {
+  if (!p) return fail("null plan");
+  if (!jpat || !hpat) return fail("exa_eval_set_compressed_host: both patterns are required");
+  DeviceGuard dguard(p->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  ExaWorkspace* w = ws ? ws : p->dflt;
+  {
+    std::lock_guard<std::mutex> lazy(w->mu);
+    if (int rc_ = ws_staging(p, w)) return rc_;
+    if (w->cap_Jc < jpat->nnz) {
+      cudaFree(w->dJc);
+      w->dJc = nullptr;
+      CU(cudaMalloc((void**)&w->dJc, (jpat->nnz > 0 ? jpat->nnz : 1) * sizeof(double)));
+      w->cap_Jc = jpat->nnz;
+    }
+    if (w->cap_Hc < hpat->nnz) {
+      cudaFree(w->dHc);
+      w->dHc = nullptr;
+      CU(cudaMalloc((void**)&w->dHc, (hpat->nnz > 0 ? hpat->nnz : 1) * sizeof(double)));
+      w->cap_Hc = hpat->nnz;
+    }
+  }
+  if (p->nvar) CU(cudaMemcpyAsync(w->dx, x, p->nvar * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (p->ncon) CU(cudaMemcpyAsync(w->dy, mult, p->ncon * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (int rc = set_compressed(p, w, jpat, hpat, w->dx, w->dy, w_obj, w->dc, w->dJc, w->dHc, st)) return rc;
+  if (p->ncon) CU(cudaMemcpyAsync(c, w->dc, p->ncon * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (jpat->nnz) CU(cudaMemcpyAsync(jac_c, w->dJc, jpat->nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (hpat->nnz) CU(cudaMemcpyAsync(hess_c, w->dHc, hpat->nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (pageable(c) || pageable(jac_c) || pageable(hess_c) || pageable(x) || pageable(mult))
+    CU(cudaStreamSynchronize(st));  // pageable copies: complete on return
+  return 0;
 }
 
 int exa_eval_cons(ExaPlan* p, ExaWorkspace* ws, const double* x, double* c, exa_stream_t stream) {

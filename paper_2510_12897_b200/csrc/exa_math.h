@@ -223,7 +223,11 @@ EXA_FN int exa_sincos_fast(double ax, double* s_out, double* c_out) {
  * double-double evaluation and platform fallback must not shape the register
  * allocation (spills, call frames) of the inlined fast path. */
 #if defined(__CUDACC_RTC__) || defined(__CUDACC__)
+#if defined(EXA_SC_SLOW_INLINE)
+__device__ __forceinline__
+#else
 __device__ __noinline__
+#endif
 #else
 static
 #endif

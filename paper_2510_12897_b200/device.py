@@ -28,7 +28,7 @@ import threading
 import numpy as np
 
 from . import _lib
-from .codegen import PatternCode
+from .codegen import _DERIV_ZERO_ELISION, PatternCode
 from .core import ModelError
 from .jit import PDL, PERSIST, THREADS_ENV, THREADS_HEAVY, choose_threads, compile_module, module_source
 
@@ -121,9 +121,10 @@ def _const_op(v: float):
     return (OP_CONST, int(np.float64(v).view(np.int64)), 0)
 
 
-def collect_patterns(plan):
+def collect_patterns(plan, relax: bool | None = None):
     """Distinct tape patterns of a plan (first-appearance order) and the
-    pattern id of every term (objective terms first, then constraint-side)."""
+    pattern id of every term (objective terms first, then constraint-side);
+    ``relax`` = zero-sign mode of the generated code (None = default)."""
     keys: dict = {}
     pcodes: list = []
     term_pid = []
@@ -138,7 +139,7 @@ def collect_patterns(plan):
         if pid is None:
             pid = len(pcodes)
             keys[key] = pid
-            pc = PatternCode(pid, tape, len(tape.field_names), len(tape.index_names), key[1])
+            pc = PatternCode(pid, tape, len(tape.field_names), len(tape.index_names), key[1], relax=relax)
             if pc.has_checks and len(tape.instr) > 4095:
                 raise ModelError("domain-checked kernels are limited to 4095 instructions")
             pcodes.append(pc)
@@ -283,15 +284,19 @@ def _bucket_layout(base_tp, augs, nvar):
 class HostLayout:
     """Everything the device needs for one plan, built on the host only."""
 
-    def __init__(self, plan, group_max: int | None = None):
+    def __init__(self, plan, group_max: int | None = None, exact_zero_sign: bool | None = None):
         self.plan = plan
         self.env_sig = (THREADS_ENV, THREADS_HEAVY, PDL)
         self.group_max_req = group_max
+        # zero-sign mode: exact = the reference's signs of zero and w * 0
+        # NaN propagation, bit for bit; relaxed = +0.0 structural zeros
+        self.relax = _DERIV_ZERO_ELISION if exact_zero_sign is None else not exact_zero_sign
+        self.exact_zero_sign = not self.relax
         terms = plan.obj_terms + plan.con_terms
         self.terms = terms
         n_obj = len(plan.obj_terms)
         self.n_obj = n_obj
-        self.patterns, self.term_pid = collect_patterns(plan)
+        self.patterns, self.term_pid = collect_patterns(plan, relax=self.relax)
         self.has_checks = any(pc.has_checks for pc in self.patterns)
         pcs = self.patterns
 
@@ -659,13 +664,23 @@ class HostLayout:
         return self.segs[m]
 
     def _host_fill(self, terms):
-        """Runs of raw J / H slots whose value is the same constant for every
-        record and every call (constant Jacobian slots; structural-zero Hessian
-        pairs, +0.0 under the zero-sign relaxation) as int64 triples (first
-        slot, length, value bits), adjacent equal runs merged.  The host path
-        fills them into the caller's arrays and copies only the rest over
-        PCIe; the kernels still write them (device callers get every slot)."""
-        runs_j, runs_h = [], []
+        """Runs of raw J / H slots the host path writes on the host instead of
+        copying them from the device (the kernels still write them: device
+        callers get every slot).
+
+        * constant runs, int64 triples (first slot, length, value bits):
+          constant Jacobian slots and -- under the zero-sign relaxation -- the
+          structural-zero Hessian pairs (+0.0); adjacent equal runs merged;
+        * exact zero-sign mode: *weighted-zero* runs, int64 quadruples (first
+          H slot, length, offset into ``wz_rows`` or -1 for the objective
+          weight, bits of the structural constant z): slot i of the run is
+          ``mult[wz_rows[off + i]] * z`` (or ``obj_weight * z``), the
+          reference's ``weight * 0.0`` with its sign and NaN propagation
+          (autodiff.py:652), computed from the caller's host multipliers.
+        """
+        runs_j, runs_h, runs_w = [], [], []
+        rows_pool, rows_off = [], {}
+        at = 0
         for t, tp in enumerate(terms):
             pc = self.patterns[self.term_pid[t]]
             d, n = self.descs[t], tp.nrec
@@ -676,6 +691,16 @@ class HostLayout:
                     runs_j.append((d["jac0"] + s_ * n, n, int(np.float64(v).view(np.int64))))
             for pr in pc.hzero:
                 runs_h.append((d["hess0"] + pr * n, n, 0))
+            for pr, z in pc.hzero_w:
+                if tp.kind == "objective":
+                    off = -1
+                else:
+                    off = rows_off.get(t)
+                    if off is None:
+                        off = rows_off[t] = at
+                        rows_pool.append(np.asarray(tp.rows, dtype=np.int32))
+                        at += n
+                runs_w.append((d["hess0"] + pr * n, n, off, int(np.float64(z).view(np.int64))))
 
         def merge(runs):
             out = []
@@ -686,6 +711,8 @@ class HostLayout:
                     out.append([a, n, v])
             return np.array(out, dtype=np.int64).reshape(-1, 3)
 
+        self.fill_wzero = np.array(sorted(runs_w), dtype=np.int64).reshape(-1, 4)
+        self.wz_rows = (np.concatenate(rows_pool) if rows_pool else np.zeros(0, dtype=np.int32)).astype(np.int32)
         return merge(runs_j), merge(runs_h)
 
     def _grad_csr(self, nvar):
@@ -713,19 +740,21 @@ class HostLayout:
         return ptr, ent
 
 
-def host_layout(plan, group_max: int | None = None) -> HostLayout:
+def host_layout(plan, group_max: int | None = None, exact_zero_sign: bool | None = None) -> HostLayout:
     """The plan's device layout (cached on the plan); ``group_max`` overrides
-    the automatic term-group size (the strided-batch plan uses 2)."""
-    if group_max is None:
+    the automatic term-group size (the strided-batch plan uses 2),
+    ``exact_zero_sign`` the default zero-sign mode."""
+    exact = (not _DERIV_ZERO_ELISION) if exact_zero_sign is None else bool(exact_zero_sign)
+    if group_max is None and exact == (not _DERIV_ZERO_ELISION):
         lay = getattr(plan, "_exa_layout", None)
         if lay is None or lay.env_sig != (THREADS_ENV, THREADS_HEAVY, PDL):
             lay = HostLayout(plan)
             plan._exa_layout = lay
         return lay
     cache = plan.__dict__.setdefault("_exa_layouts", {})
-    key = (THREADS_ENV, THREADS_HEAVY, PDL, group_max)
+    key = (THREADS_ENV, THREADS_HEAVY, PDL, group_max, exact)
     if key not in cache:
-        cache[key] = HostLayout(plan, group_max)
+        cache[key] = HostLayout(plan, group_max, exact_zero_sign=exact)
     return cache[key]
 
 
@@ -742,7 +771,7 @@ def precompile(plan) -> bytes:
 class DevicePlan:
     """The model's plan resident on one GPU, with its compiled kernels."""
 
-    def __init__(self, model, device=None, group_max: int | None = None):
+    def __init__(self, model, device=None, group_max: int | None = None, exact_zero_sign: bool | None = None):
         import torch
 
         if not torch.cuda.is_available():
@@ -751,8 +780,9 @@ class DevicePlan:
         plan = model.plan
         self.model = model
         self.plan = plan
-        lay = host_layout(plan, group_max)
+        lay = host_layout(plan, group_max, exact_zero_sign)
         self.layout = lay
+        self.exact_zero_sign = lay.exact_zero_sign
         self.patterns = lay.patterns
         self.has_checks = lay.has_checks
         self.n_ctas = lay.n_ctas
@@ -801,6 +831,12 @@ class DevicePlan:
         self._fill = np.ascontiguousarray(np.concatenate([lay.fill_jac, lay.fill_hess]).reshape(-1), dtype=np.int64)
         desc.host_fill = self._fill.ctypes.data_as(C.POINTER(C.c_int64))
         desc.n_fill_jac, desc.n_fill_hess = len(lay.fill_jac), len(lay.fill_hess)
+        self._wz = np.ascontiguousarray(lay.fill_wzero.reshape(-1), dtype=np.int64)
+        self._wz_rows = np.ascontiguousarray(lay.wz_rows, dtype=np.int32)
+        desc.host_wzero = self._wz.ctypes.data_as(C.POINTER(C.c_int64))
+        desc.n_wzero = len(lay.fill_wzero)
+        desc.host_wzero_rows = self._wz_rows.ctypes.data_as(C.POINTER(C.c_int32))
+        desc.n_wzero_rows = self._wz_rows.size
         n_obj, n_con = len(plan.obj_terms), len(plan.con_terms)
         bases = {
             _lib.MODE_SET: (n_con, 0), _lib.MODE_CONS: (0, 0), _lib.MODE_JAC: (0, 0),

@@ -48,6 +48,9 @@ def choose_threads(n_threads: int) -> int:
 def min_blocks(threads: int) -> int:
     return int(MINB_ENV) if MINB_ENV is not None else max(1, 1024 // threads)
 SC_TABLE = os.environ.get("EXA_SC_TABLE", "global")  # sin/cos table: "global" (L1/L2) or "const"
+# sin/cos slow path (Ziv's rare fallback) inline behind a warp-uniform branch
+# instead of an out-of-line call (whose ABI spills live values around it)
+SC_SLOW_INLINE = os.environ.get("EXA_SC_SLOW_INLINE", "0") == "1"
 SINCOS_IMPL = os.environ.get("EXA_SINCOS_IMPL", "cr")  # "cuda" = libdevice sincos, NOT parity-exact
 # Persistent specialised kernels (experiment, off): each real CTA runs PERSIST
 # virtual CTAs of THREADS threads side by side and strides over the model's
@@ -396,7 +399,7 @@ __device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, con
         augs = [(layout.patterns[layout.term_pid[u]], off, m, s_)
                 for (u, off, m, s_) in getattr(layout, "group_augs", {}).get(gid, [])]
         out.append(group_source(gid, [(layout.patterns[layout.term_pid[u]], mem) for u, mem in zip(grp, members)],
-                                augs))
+                                augs, relax=layout.relax))
     for m, name in enumerate(KERNEL_NAMES):
         for half, suffix in ((0, "_h"), (1, "_l")):
             out.append(_kernel_source(layout, m, half, name + suffix))
@@ -681,6 +684,7 @@ def module_source(patterns, layout=None, threads: int = 32) -> str:
              f"#define EXA_PDL_MID {PDL_MID}",
              f"#define EXA_TRACE {1 if TRACE else 0}",
              "#define EXA_SC_CONST 1" if SC_TABLE == "const" else "",
+             "#define EXA_SC_SLOW_INLINE 1" if SC_SLOW_INLINE else "",
              f"#define EXA_TRACE_NT {max(threads, THREADS_HEAVY) * max(1, PERSIST)}",
              _inline_header("exa_device.h", seen), _inline_header("exa_math.h", seen), _PRELUDE]
     if SINCOS_IMPL == "cuda":

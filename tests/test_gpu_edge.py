@@ -10,7 +10,7 @@ from oracle import tape_oracle as O
 from paper_2510_12897_b200 import (DataTable, EvalDomainError, ModelCore, cos, eval_callback_set,
                                    eval_constraints, eval_gradient, eval_hessian, eval_jacobian,
                                    eval_objective, field, sin)
-from test_gpu_parity import bitwise_equal
+from oracle.parity import ieee_equal
 
 pytestmark = pytest.mark.gpu
 
@@ -31,20 +31,20 @@ def _check_all(model, seed=0):
     J = np.empty(model.plan.n_jac_slots)
     H = np.empty(model.plan.n_hess_slots)
     eval_callback_set(model, x, y, 0.5, c, J, H)
-    assert bitwise_equal(c, c0) and bitwise_equal(J, J0) and bitwise_equal(H, H0)
+    assert ieee_equal(c, c0) and ieee_equal(J, J0) and ieee_equal(H, H0)
     c2 = np.empty(model.ncon)
     if model.ncon:
         eval_constraints(model, x, c2)
-        assert bitwise_equal(c2, c0)
+        assert ieee_equal(c2, c0)
     J2 = np.empty(model.plan.n_jac_slots)
     eval_jacobian(model, x, J2)
-    assert bitwise_equal(J2, J0)
+    assert ieee_equal(J2, J0)
     H2 = np.empty(model.plan.n_hess_slots)
     eval_hessian(model, x, y, 0.5, H2)
-    assert bitwise_equal(H2, H0)
+    assert ieee_equal(H2, H0)
     g = np.empty(model.nvar)
     eval_gradient(model, x, g)
-    assert bitwise_equal(g, g0)
+    assert ieee_equal(g, g0)
     assert eval_objective(model, x) == f0
 
 

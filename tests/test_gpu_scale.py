@@ -14,7 +14,7 @@ import pytest
 
 from oracle import crtrig
 from oracle import tape_oracle as O
-from test_gpu_parity import bitwise_equal, strict_violations
+from oracle.parity import bit_equal, ieee_equal, strict_violations, zero_sign_mismatches
 
 pytestmark = pytest.mark.gpu
 
@@ -31,35 +31,48 @@ def workload(name):
 
 
 def _gpu_set(model, x, y, w):
+    """One fused set through the zero-copy torch path (device buffers)."""
+    import torch
+
     from paper_2510_12897_b200 import eval_callback_set
 
-    c = np.empty(model.ncon)
-    J = np.empty(model.plan.n_jac_slots)
-    H = np.empty(model.plan.n_hess_slots)
-    eval_callback_set(model, x, y, w, c, J, H)
-    return c, J, H
+    dev = torch.device("cuda", 0)
+    out = [torch.full((n,), float("nan"), dtype=torch.float64, device=dev)
+           for n in (model.ncon, model.plan.n_jac_slots, model.plan.n_hess_slots)]
+    eval_callback_set(model, torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev), w, *out)
+    return tuple(t.cpu().numpy() for t in out)
 
 
-@pytest.mark.parametrize("name", ["case1354", "case13659", "mp96_case1354", "scen96_case1354"])
+# strict 1e-12 violations against the numpy oracle (= the reference's
+# arithmetic) recorded by tools/parity_report.py at this evaluation point
+# (profiles/parity_r02.json): every one is glibc sin/cos misrounding amplified
+# by cancellation, i.e. equal to the CR-trig oracle
+RECORDED_STRICT = {"case1354": (0, 0, 0), "case13659": (0, 0, 0), "mp96_case1354": (0, 0, 0),
+                   "scen96_case1354": (0, 0, 0), "n1_case2000": (3, 2, 0)}
+
+
+@pytest.mark.parametrize("name", ["case1354", "case13659", "mp96_case1354", "scen96_case1354", "n1_case2000"])
 def test_set_parity_at_scale(name):
+    """n1_case2000 is north_star config 5 at its stated size: 1024
+    contingencies of the case2000-shaped network (4.5 GB of outputs)."""
     model, (x, y, w) = workload(name)
     got = _gpu_set(model, x, y, w)
-    ref = O.eval_set(model.plan, x, y, w)
+    exact = model.device_plan.exact_zero_sign
     O.use_trig(crtrig.TRIG)
     try:
         cr = O.eval_set(model.plan, x, y, w)
     finally:
         O.use_trig(None)
-    report = {}
-    for label, a, r, o in zip(("cons", "jac", "hess"), got, ref, cr):
-        assert bitwise_equal(a, o), f"{name}/{label}: differs from CR-trig oracle"
+    for label, a, o in zip(("cons", "jac", "hess"), got, cr):
+        # bit for bit (signs of zero included) in the exact zero-sign mode
+        assert (bit_equal if exact else ieee_equal)(a, o), f"{name}/{label}: differs from CR-trig oracle"
+    del cr
+    ref = O.eval_set(model.plan, x, y, w)
+    for k, (label, a, r) in enumerate(zip(("cons", "jac", "hess"), got, ref)):
         bad = strict_violations(a, r)
-        assert bitwise_equal(a[bad], o[bad])
-        report[label] = (int(bad.size), int((a != r).sum()), a.size)
-    # the deviations are rare: at most a few per 10^5 entries
-    for label, (nbad, ndiff, n) in report.items():
-        assert nbad <= max(3, n // 20000), (label, nbad, n)
-    print(name, report)
+        assert bad.size <= RECORDED_STRICT[name][k], (name, label, bad.size)
+        if exact:
+            assert zero_sign_mismatches(a, r) == 0
 
 
 @pytest.mark.parametrize("name", ["case13659"])
@@ -73,7 +86,7 @@ def test_objective_gradient_at_scale(name):
     eval_gradient(model, x, g)
     go = np.empty(model.nvar)
     O.eval_gradient(model.plan, x, go)
-    assert bitwise_equal(g, go)
+    assert ieee_equal(g, go)
 
 
 def test_hessian_linear_in_multipliers_at_scale():
@@ -98,8 +111,8 @@ def test_compressed_hessian_at_scale():
     c, J, H = _gpu_set(model, x, y, w)
     hp = compress_coordinates(*hessian_structure(model))
     r, cc, smap = O.compress(model.plan.hess_rows, model.plan.hess_cols)
-    assert bitwise_equal(hp.rows, r) and bitwise_equal(hp.cols, cc)
-    assert bitwise_equal(hp.sum_values(H), O.sum_values(smap, r.size, H))
+    assert ieee_equal(hp.rows, r) and ieee_equal(hp.cols, cc)
+    assert ieee_equal(hp.sum_values(H), O.sum_values(smap, r.size, H))
 
 
 def test_scopf_batch_gpu_parity():
@@ -117,9 +130,9 @@ def test_scopf_batch_gpu_parity():
         O.use_trig(None)
     ref = O.eval_set(model.plan, x, y, w)
     for a, o, r in zip(got, cr, ref):
-        assert bitwise_equal(a, o)
+        assert ieee_equal(a, o)
         bad = strict_violations(a, r)
-        assert bitwise_equal(a[bad], o[bad])
+        assert ieee_equal(a[bad], o[bad])
 
 
 def test_period_shards_on_gpu_reassemble_global():
@@ -139,4 +152,4 @@ def test_period_shards_on_gpu_reassemble_global():
         sh = attach_maps(mpopf_shard(case, curve, r, 3), gm)
         sc, sJ, sH = _gpu_set(sh.model, x[sh.var_map], y[sh.row_map], w)
         c[sh.row_map], J[sh.jac_map], H[sh.hess_map] = sc, sJ, sH
-    assert bitwise_equal(c, gc) and bitwise_equal(J, gJ) and bitwise_equal(H, gH)
+    assert ieee_equal(c, gc) and ieee_equal(J, gJ) and ieee_equal(H, gH)
