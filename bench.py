@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="headline and e2e only")
-    ap.add_argument("--sharded-legs", action="store_true", help="run the sharded MP96 / N-1 legs at N = 1 too")
+    ap.add_argument("--sharded-legs", action="store_true", help="(no-op: the other configs always run unless --no-extras)")
     return ap.parse_args()
 
 
@@ -370,10 +370,13 @@ def isolated_latency_us(launch, stream, dev, n=40):
     return statistics.median(out[5:])
 
 
-def sharded_leg(name, rank, ws, local, n_sets=8, steps=5):
-    """One config sharded over the ranks (strong scaling): this rank's shard
-    of ONE instance, timed sets (max over ranks), plus one ShardComm.exchange
-    round (NCCL P2P halo) and one objective reduction (NCCL all-gather)."""
+def sharded_leg(name, rank, ws, local, n_sets=8, steps=5, peak=None):
+    """One BASELINE config measured in this run.  At N > 1 a batched config is
+    sharded over the ranks (strong scaling): this rank's shard of ONE
+    instance, timed sets (max over ranks), plus one ShardComm.exchange round
+    (NCCL P2P halo) and one objective reduction (NCCL all-gather).  At N = 1
+    it is the whole instance on this GPU (the config's own bench line, as an
+    extra key of the headline run)."""
     import numpy as np
     import torch
 
@@ -381,22 +384,27 @@ def sharded_leg(name, rank, ws, local, n_sets=8, steps=5):
     from paper_2510_12897_b200.distributed import mpopf_comm, scopf_comm
     from paper_2510_12897_b200.sharding import mpopf_shard
     from paper_2510_12897_b200.synth import demand_curve, pglib_shaped
-    from paper_2510_12897_b200.workloads import build_workload, model_summary, n1_contingencies
+    from paper_2510_12897_b200.workloads import (build_workload, model_summary, n1_contingencies,
+                                                 scenario_factors)
 
     dev = torch.device("cuda", local)
     t_build = time.perf_counter()
-    head, base = name.split("_", 1)
     comm = None
-    if head.startswith("n1"):
-        model = build_workload(name, lower_to_gpu=False, rank=rank, world=ws)
-        n_inst = len(n1_contingencies(pglib_shaped(base, seed=1), int(head[2:] or 1024))) + 1
-        if ws > 1:
-            comm = scopf_comm(model, n_inst, rank, ws)
+    if ws == 1 or "_" not in name:
+        model = build_workload(name, lower_to_gpu=False)
     else:
-        T = int(head[2:])
-        shard = mpopf_shard(pglib_shaped(base, seed=1), demand_curve(T), rank, ws, 0.25, lower_to_gpu=False)
-        model = shard.model
-        if ws > 1:
+        head, base = name.split("_", 1)
+        if head.startswith("n1"):
+            model = build_workload(name, lower_to_gpu=False, rank=rank, world=ws)
+            n_inst = len(n1_contingencies(pglib_shaped(base, seed=1), int(head[2:] or 1024))) + 1
+            comm = scopf_comm(model, n_inst, rank, ws)
+        else:
+            scen = head.startswith("scen")
+            T = int(head[4:] if scen else head[2:])
+            prof = scenario_factors(T) if scen else demand_curve(T)
+            shard = mpopf_shard(pglib_shaped(base, seed=1), prof, rank, ws, None if scen else 0.25,
+                                lower_to_gpu=False)
+            model = shard.model
             comm = mpopf_comm(shard, T, False, rank, ws)
     summ = model_summary(model)
     R = max(2, min(8, int(np.ceil(2 * L2_BYTES / summ["bytes_per_set"]))))
@@ -435,6 +443,8 @@ def sharded_leg(name, rank, ws, local, n_sets=8, steps=5):
                    comm_note="wall time per call incl. host launch, max over ranks")
     out.update(value=1e6 / us, unit="sets/s of the whole instance (every rank's shard per set)",
                max_rank_us_per_set=us, n_ranks=ws)
+    if peak:
+        out["roofline_frac"] = summ["bytes_per_set"] / us / 1e3 / peak  # this rank's shard bytes / its time
     del plans, bufs
     torch.cuda.empty_cache()
     return out
@@ -455,8 +465,8 @@ def compressed_leg(model, plans, bufs, lib, stream, dev, peak):
 
     jp, hp = model_patterns(model)
     R = len(plans)
-    hj = [jp.device_handle(p) for p in plans]
-    hh = [hp.device_handle(p) for p in plans]
+    hj = [jp.device_handle(p, "jac") for p in plans]
+    hh = [hp.device_handle(p, "hess") for p in plans]
     for b in bufs:
         b["Jc"] = torch.empty(jp.nnz, dtype=torch.float64, device=dev)
         b["Hc"] = torch.empty(hp.nnz, dtype=torch.float64, device=dev)
@@ -699,8 +709,12 @@ def main():
 
     # ---- sharded configs over the ranks (multi-GPU readiness, strong scaling)
     sharded_out = None
-    if not sharded and (ws > 1 or args.sharded_legs):
-        sharded_out = [sharded_leg(name, rank, ws, local) for name in ("mp96_case1354", "n1_case2000")]
+    if not sharded and not args.no_extras:
+        # the other BASELINE configs, measured in this run: at N = 1 each whole
+        # instance on this GPU, at N > 1 the batched ones sharded over the ranks
+        names = (("case1354", "mp96_case1354", "scen96_case1354", "n1_case2000") if ws == 1
+                 else ("mp96_case1354", "scen96_case1354", "n1_case2000"))
+        sharded_out = [sharded_leg(name, rank, ws, local, peak=peak) for name in names]
 
     # ---- end to end: host buffers through the C ABI, copies inside the timed region.
     # exa_eval_set_host = H2D(x, y) + set kernel + D2H(c, J, H) on one stream;
@@ -836,7 +850,7 @@ def main():
         "clocks": sampler.summary(),
         "batched": batched,
         **extras,
-        "sharded": sharded_out,
+        "configs": sharded_out,
         "gpu_launches": args.steps * S,
         "kernel_regs": info["regs_set_kernel"],
     }

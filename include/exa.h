@@ -207,6 +207,16 @@ int exa_eval_hess_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, co
 typedef struct ExaPattern ExaPattern;
 int exa_pattern_create(ExaPlan* plan, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
                        ExaPattern** out);
+/* The same, told which raw slots the plan's set kernel writes as the same
+ * constant on every call (known[r] != 0: raw slot r always holds
+ * known_val[r]; the plan's constant Jacobian slots and, under the zero-sign
+ * relaxation, its structural-zero Hessian pairs -- HostLayout fill runs).
+ * The compressed sum then skips known +0.0 slots (exact: a fold that starts
+ * at +0.0 never holds -0.0) and takes known constants from the pattern
+ * instead of gathering them; valid only with exa_eval_set_compressed on a
+ * plan whose kernels write those values. */
+int exa_pattern_create_known(ExaPlan* plan, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
+                             const uint8_t* known, const double* known_val, ExaPattern** out);
 void exa_pattern_destroy(ExaPattern* pattern);
 /* cons + COMPRESSED Jacobian and Hessian values of one point: the set kernel
  * writes the raw slots into the workspace's scratch and the two segmented

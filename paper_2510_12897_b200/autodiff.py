@@ -384,20 +384,41 @@ class CompressedPattern:
         self._dev_csr = cache
         return cache
 
-    def device_handle(self, dp):
-        """The pattern as an ``ExaPattern`` on ``dp``'s device (created once)."""
+    def device_handle(self, dp, kind: str | None = None):
+        """The pattern as an ``ExaPattern`` on ``dp``'s device (created once).
+
+        ``kind`` = ``"jac"`` / ``"hess"``: this is the model's own J / H
+        pattern, evaluated by ``exa_eval_set_compressed`` on ``dp``; the slots
+        ``dp``'s kernels write as the same constant on every call (its
+        layout's fill runs: constant J slots, relaxed structural-zero H pairs)
+        are then folded from the pattern instead of gathered (+0.0 skipped).
+        Every plan of one model with the same zero-sign mode has the same
+        runs, so the handle is shared by them."""
         handles = self.__dict__.setdefault("_exa_handles", {})
-        h = handles.get(dp.device)
+        key = (dp.device, kind, bool(dp.exact_zero_sign) if kind else None)
+        h = handles.get(key)
         if h is None:
             order = np.argsort(self.slot_map, kind="stable")
             ptr = np.zeros(self.nnz + 1, dtype=np.int64)
             np.cumsum(np.bincount(self.slot_map, minlength=self.nnz), out=ptr[1:])
             ent = np.ascontiguousarray(order.astype(np.int32))
             h = C.c_void_p()
-            _lib.check(dp._lib.exa_pattern_create(dp.handle, int(self.slot_map.size), self.nnz,
-                                                  ptr.ctypes.data, ent.ctypes.data, C.byref(h)),
-                       "exa_pattern_create")
-            handles[dp.device] = h
+            if kind is None:
+                _lib.check(dp._lib.exa_pattern_create(dp.handle, int(self.slot_map.size), self.nnz,
+                                                      ptr.ctypes.data, ent.ctypes.data, C.byref(h)),
+                           "exa_pattern_create")
+            else:
+                runs = dp.layout.fill_jac if kind == "jac" else dp.layout.fill_hess
+                known = np.zeros(self.slot_map.size, dtype=np.uint8)
+                val = np.zeros(self.slot_map.size, dtype=np.int64)
+                for a, n, bits in runs:
+                    known[a:a + n] = 1
+                    val[a:a + n] = bits
+                _lib.check(dp._lib.exa_pattern_create_known(dp.handle, int(self.slot_map.size), self.nnz,
+                                                            ptr.ctypes.data, ent.ctypes.data, known.ctypes.data,
+                                                            val.ctypes.data, C.byref(h)),
+                           "exa_pattern_create_known")
+            handles[key] = h
         return h
 
     def __del__(self):
@@ -467,7 +488,7 @@ def eval_callback_set_compressed(model, x, mult, obj_weight: float, out_c, out_j
         if _shape(buf) != (n,):
             raise ValueError(f"{what} buffer has shape {_shape(buf)}, expected ({n},)")
     dp = _dplan(model)
-    jh, hh = jp.device_handle(dp), hp.device_handle(dp)
+    jh, hh = jp.device_handle(dp, "jac"), hp.device_handle(dp, "hess")
     if not _is_cuda(x) and not _is_cuda(mult) and _host_outputs(out_c, out_jac, out_hess):
         return _host_call(dp, "exa_eval_set_compressed_host", "set", jh, hh, x, mult, float(obj_weight),
                           out_c, out_jac, out_hess)

@@ -23,6 +23,8 @@
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
+#include <set>
+#include <unordered_map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -112,6 +114,7 @@ struct ExaPlan {
   int64_t n_vscr = 0, n_gscr = 0;
   int64_t* leaves = nullptr;
   int32_t n_leaves = 0;
+  int64_t obj_leaf_max = 0; /* longest pairwise leaf (numpy: <= 128) */
   int64_t* prog = nullptr;
   int32_t n_prog = 0;
   int64_t* grad_ptr = nullptr;
@@ -141,8 +144,27 @@ struct ExaPlan {
 struct ExaPattern {
   int device = 0;
   int64_t n_raw = 0, nnz = 0;
-  int64_t* ptr = nullptr;
-  int32_t* ent = nullptr;
+  /* CTA chunks of the compressed sum.  Each entry's raw slots, in increasing
+     slot order, minus the slots known to hold +0.0 on every call (dropping
+     them from a fold that starts at +0.0 is exact), form its *stage*; chunk b
+     covers entries [chk[b], chk[b+1]) whose stages fit one CTA's shared
+     memory (cap = 256 * ipt slots, at most cap entries) -- or a single
+     longer entry.  Per chunk: gathered
+     slots [che[b], che[b+1]) of src (raw slot id) / dst (stage position),
+     sorted by src so that a warp's gathers hit runs of consecutive raw slots;
+     known constant slots [chc[b], chc[b+1]) of cpos (stage position) / cid
+     (index into cval).  Per entry: est = start of its stage.  A long entry
+     keeps every non-skipped slot in src, in slot order. */
+  int32_t nch = 0, ipt = 8;
+  int32_t* chk = nullptr;
+  int32_t* che = nullptr;
+  int32_t* chc = nullptr;
+  int32_t* src = nullptr;
+  uint16_t* dst = nullptr;
+  uint16_t* cpos = nullptr;
+  uint16_t* cid = nullptr;
+  uint16_t* est = nullptr;
+  double* cval = nullptr;
 };
 
 // ---------------------------------------------------------------------------
@@ -209,6 +231,90 @@ __global__ void exa_obj_combine(const int64_t* __restrict__ prog, int n_prog,
   *out = total;
 }
 
+// The same objective sum as exa_obj_leaves + exa_obj_combine in one CTA, for
+// programs whose leaf sums and opcodes fit shared memory: the combine program
+// is staged in shared memory by all threads, each warp reduces leaves (lanes
+// load the leaf's <= 128 values at once into a warp buffer, lane 0 replays
+// numpy's accumulator order from it), then thread 0 runs the program.  One
+// launch and no chain of dependent global loads (the two-kernel path spent
+// ~20 us at case13659 on the single thread's prog/leaf loads).
+#define EXA_OBJ_THREADS 512
+#define EXA_OBJ_LEAF_MAX 128
+__global__ void __launch_bounds__(EXA_OBJ_THREADS) exa_obj_fused(const double* __restrict__ V,
+                                                                 const int64_t* __restrict__ leaves, int n_leaves,
+                                                                 const int64_t* __restrict__ prog, int n_prog,
+                                                                 double* __restrict__ out) {
+  extern __shared__ double osm[];
+  double* wbuf = osm;                                            // [warps][EXA_OBJ_LEAF_MAX]
+  double* ls = wbuf + (EXA_OBJ_THREADS / 32) * EXA_OBJ_LEAF_MAX;  // [n_leaves]
+  int64_t* sprog = reinterpret_cast<int64_t*>(ls + n_leaves);    // [n_prog][2]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < n_prog; i += EXA_OBJ_THREADS) {
+    sprog[2 * i] = __ldg(prog + 3 * i);
+    sprog[2 * i + 1] = __ldg(prog + 3 * i + 1);
+  }
+  double* wb = wbuf + warp * EXA_OBJ_LEAF_MAX;
+  for (int l = warp; l < n_leaves; l += EXA_OBJ_THREADS / 32) {
+    const double* a = V + __ldg(leaves + 2 * l);
+    const int n = (int)__ldg(leaves + 2 * l + 1);
+#pragma unroll
+    for (int j = 0; j < EXA_OBJ_LEAF_MAX / 32; ++j)
+      if (lane + 32 * j < n) wb[lane + 32 * j] = a[lane + 32 * j];
+    __syncwarp();
+    if (lane == 0) {
+      double res;
+      if (n < 8) {
+        res = 0.0;
+        for (int i = 0; i < n; ++i) res = res + wb[i];
+      } else {
+        double r0 = wb[0], r1 = wb[1], r2 = wb[2], r3 = wb[3], r4 = wb[4], r5 = wb[5], r6 = wb[6], r7 = wb[7];
+        int i = 8;
+        for (; i < n - (n % 8); i += 8) {
+          r0 = r0 + wb[i + 0];
+          r1 = r1 + wb[i + 1];
+          r2 = r2 + wb[i + 2];
+          r3 = r3 + wb[i + 3];
+          r4 = r4 + wb[i + 4];
+          r5 = r5 + wb[i + 5];
+          r6 = r6 + wb[i + 6];
+          r7 = r7 + wb[i + 7];
+        }
+        res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+        for (; i < n; ++i) res = res + wb[i];
+      }
+      ls[l] = res;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (tid != 0) return;
+  double stack[EXA_OBJ_STACK];
+  int sp = 0;
+  double total = 0.0;
+  for (int q = 0; q < n_prog; ++q) {
+    const int64_t op = sprog[2 * q], a = sprog[2 * q + 1];
+    switch ((int)op) {
+      case OP_LEAF: stack[sp++] = ls[a]; break;
+      case OP_ADD: {
+        const double b = stack[--sp];
+        const double x = stack[--sp];
+        stack[sp++] = x + b;
+        break;
+      }
+      case OP_CONST: stack[sp++] = __longlong_as_double((long long)a); break;
+      case OP_ZERO_PLUS: stack[sp - 1] = 0.0 + stack[sp - 1]; break;
+      case OP_TOTAL_ADD: total = total + stack[--sp]; break;
+      default: break;
+    }
+  }
+  *out = total;
+}
+#define EXA_OBJ_FUSED_SMEM_MAX (160 * 1024)
+static size_t obj_fused_smem(int n_leaves, int n_prog) {
+  return sizeof(double) * ((EXA_OBJ_THREADS / 32) * EXA_OBJ_LEAF_MAX + (size_t)n_leaves) +
+         2 * sizeof(int64_t) * (size_t)n_prog;
+}
+
 // Stack depth of an objective combine program, or -1 if it is malformed
 // (unknown opcode, pop from an empty stack, leaf index out of range).
 static int prog_depth(const int64_t* prog, int n_prog, int n_leaves) {
@@ -253,41 +359,100 @@ __global__ void exa_grad_reduce(int64_t nvar, const int64_t* __restrict__ ptr, c
 }
 
 // compressed[k] = 0 + sum of raw slots mapped to k, in slot order (np.bincount).
+// The raw loads of an entry are issued together (8 at a time) before the
+// in-order adds, so a long segment costs a few load latencies, not one each.
 __global__ void exa_compress_reduce(int64_t nnz, const int64_t* __restrict__ ptr, const int32_t* __restrict__ ent,
                                     const double* __restrict__ raw, double* __restrict__ out) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nnz) return;
   double acc = 0.0;
   const int64_t e1 = ptr[k + 1];
-  for (int64_t e = ptr[k]; e < e1; ++e) acc = acc + __ldg(raw + __ldg(ent + e));
+  int64_t e = ptr[k];
+  for (; e + 8 <= e1; e += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldg(raw + __ldg(ent + e + j));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc = acc + v[j];
+  }
+  for (; e < e1; ++e) acc = acc + __ldg(raw + __ldg(ent + e));
   out[k] = acc;
 }
 
-// Compressed J and H of one callback set in one launch (entries [0, nJ) are
-// J's, the rest H's).  Launched as a programmatic dependent of the set
-// kernel: the CTAs load their CSR ranges, then wait for the set's raw slots.
-__global__ void __launch_bounds__(256) exa_compress2_kernel(
-    int64_t nJ, const int64_t* __restrict__ ptrJ, const int32_t* __restrict__ entJ, const double* rawJ,
-    double* __restrict__ outJ, int64_t nH, const int64_t* __restrict__ ptrH, const int32_t* __restrict__ entH,
-    const double* rawH, double* __restrict__ outH) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool isJ = i < nJ;
-  const int64_t k = isJ ? i : i - nJ;
-  const bool live = isJ || k < nH;
-  const int64_t* ptr = isJ ? ptrJ : ptrH;
-  const int32_t* ent = isJ ? entJ : entH;
-  int64_t e0 = 0, e1 = 0;
-  if (live) {
-    e0 = __ldg(ptr + k);
-    e1 = __ldg(ptr + k + 1);
+// Compressed J and H of one callback set in one launch, one CTA per chunk of
+// compressed entries (chunks [0, nchJ) are J's, the rest H's).  Launched as a
+// programmatic dependent of the set kernel: before griddepcontrol.wait a CTA
+// loads its chunk's slot map and writes the known constant slots into its
+// shared-memory stage (plan data only); then it gathers the set's raw slots
+// in ADDRESS order into the stage (ENTRY order), and each thread folds its
+// entries' stages in increasing slot order (np.bincount's order: compressed[k]
+// = ((0 + r_1) + r_2) + ...) and writes them coalesced.  A chunk holding one
+// entry longer than the stage is folded by one thread from global memory.
+#define EXA_CMP_THREADS 256
+// gathers per thread (stage = 256 * IPT slots); EXA_CMP_IPT picks it when a
+// pattern is created (chunks are sized for it)
+static int cmp_ipt_env() {
+  const char* e = getenv("EXA_CMP_IPT");
+  const int v = e ? atoi(e) : 8;
+  return (v == 4 || v == 8 || v == 12 || v == 16) ? v : 8;
+}
+struct ExaCmpArgs {
+  const int32_t *chk, *che, *chc, *src;
+  const uint16_t *dst, *cpos, *cid, *est;
+  const double* cval;
+  const double* raw;
+  double* out;
+};
+template <int IPT, int MINB>
+__global__ void __launch_bounds__(EXA_CMP_THREADS, MINB) exa_compress2_kernel(int nchJ, ExaCmpArgs J, ExaCmpArgs H) {
+  constexpr int EXA_CMP_IPT = IPT;
+  constexpr int EXA_CMP_CAP = EXA_CMP_THREADS * IPT;
+  extern __shared__ double vals[];                                   // [EXA_CMP_CAP]
+  uint16_t* sst = reinterpret_cast<uint16_t*>(vals + EXA_CMP_CAP);  // [EXA_CMP_CAP + 1]
+  const int tid = threadIdx.x;
+  int b = blockIdx.x;
+  const bool isJ = b < nchJ;
+  if (!isJ) b -= nchJ;
+  const ExaCmpArgs& P = isJ ? J : H;
+  const int k0 = __ldg(P.chk + b), k1 = __ldg(P.chk + b + 1);
+  const int g0 = __ldg(P.che + b), g1 = __ldg(P.che + b + 1);
+  const int c0 = __ldg(P.chc + b), c1 = __ldg(P.chc + b + 1);
+  const int ng = g1 - g0, nc = c1 - c0, nk = k1 - k0;
+  if (ng + nc > EXA_CMP_CAP) {  // one long entry: its slots in increasing order
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (tid == 0) {
+      double acc = 0.0;
+      for (int e = g0; e < g1; ++e) acc = acc + P.raw[__ldg(P.src + e)];
+      P.out[k0] = acc;
+    }
+    return;
   }
+  int idx[EXA_CMP_IPT], pos[EXA_CMP_IPT];
+#pragma unroll
+  for (int j = 0; j < EXA_CMP_IPT; ++j) {
+    const int e = tid + EXA_CMP_THREADS * j;
+    idx[j] = e < ng ? __ldg(P.src + g0 + e) : -1;
+    pos[j] = e < ng ? (int)__ldg(P.dst + g0 + e) : 0;
+  }
+  for (int i = tid; i < nc; i += EXA_CMP_THREADS) vals[__ldg(P.cpos + c0 + i)] = __ldg(P.cval + __ldg(P.cid + c0 + i));
+  for (int i = tid; i < nk; i += EXA_CMP_THREADS) sst[i] = __ldg(P.est + k0 + i);
+  if (tid == 0) sst[nk] = (uint16_t)(ng + nc);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (!live) return;
-  const double* raw = isJ ? rawJ : rawH;
-  double acc = 0.0;
-  for (int64_t e = e0; e < e1; ++e) acc = acc + raw[__ldg(ent + e)];  // plain load: written by the set
-  (isJ ? outJ : outH)[k] = acc;
+  double v[EXA_CMP_IPT];
+#pragma unroll
+  for (int j = 0; j < EXA_CMP_IPT; ++j) v[j] = idx[j] >= 0 ? P.raw[idx[j]] : 0.0;  // plain loads: the set wrote them
+#pragma unroll
+  for (int j = 0; j < EXA_CMP_IPT; ++j)
+    if (idx[j] >= 0) vals[pos[j]] = v[j];
+  __syncthreads();
+  for (int i = tid; i < nk; i += EXA_CMP_THREADS) {
+    double acc = 0.0;
+    const int z = sst[i + 1];
+    for (int e = sst[i]; e < z; ++e) acc = acc + vals[e];
+    P.out[k0 + i] = acc;
+  }
 }
 
 // KKT assembly (reference solver.py:421-456): one thread per lower-triangle
@@ -605,6 +770,8 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
 
   p->n_leaves = d->n_leaves;
   p->n_prog = d->n_prog;
+  for (int l = 0; l < d->n_leaves; ++l)
+    if (d->leaves[2 * l + 1] > p->obj_leaf_max) p->obj_leaf_max = d->leaves[2 * l + 1];
   {
     const int depth = d->n_prog ? prog_depth(d->obj_prog, d->n_prog, d->n_leaves) : 0;
     if (depth < 0) return bail(fail("objective combine program is malformed"));
@@ -1034,9 +1201,9 @@ int exa_eval_hess_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const doub
   return host_eval(p, ws, EXA_MODE_HESS, x, mult, w_obj, nullptr, nullptr, hess, (cudaStream_t)stream);
 }
 
-int exa_pattern_create(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
-                       ExaPattern** out) {
-  if (!p || !out || n_raw < 0 || nnz < 0 || (nnz && !ptr) || (n_raw && !ent))
+int exa_pattern_create_known(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
+                             const uint8_t* known, const double* known_val, ExaPattern** out) {
+  if (!p || !out || n_raw < 0 || nnz < 0 || (nnz && !ptr) || (n_raw && !ent) || (known && !known_val))
     return fail("exa_pattern_create: invalid argument");
   *out = nullptr;
   if (ptr && (ptr[0] != 0 || ptr[nnz] != n_raw)) return fail("exa_pattern_create: ptr must run from 0 to n_raw");
@@ -1044,13 +1211,90 @@ int exa_pattern_create(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* pt
     if (ptr[k + 1] < ptr[k]) return fail("exa_pattern_create: ptr must be non-decreasing");
   for (int64_t e = 0; e < n_raw; ++e)
     if (ent[e] < 0 || ent[e] >= n_raw) return fail("exa_pattern_create: raw slot %lld out of range", (long long)e);
+  if (n_raw >= INT32_MAX) return fail("exa_pattern_create: more than 2^31 - 1 raw slots");
+  const int ipt = cmp_ipt_env(), EXA_CMP_CAP = EXA_CMP_THREADS * ipt;
+  /* per raw slot: 0 = gathered, 1 = known +0.0 (dropped), 2 = known constant */
+  auto cls = [&](int32_t r) -> int {
+    if (!known || !known[r]) return 0;
+    uint64_t bits;
+    std::memcpy(&bits, known_val + r, 8);
+    return bits == 0 ? 1 : 2;
+  };
+  std::vector<int32_t> stage_len((size_t)nnz);
+  for (int64_t k = 0; k < nnz; ++k) {
+    int32_t L = 0;
+    for (int64_t e = ptr[k]; e < ptr[k + 1]; ++e) L += cls(ent[e]) != 1;
+    stage_len[k] = L;
+  }
+  std::vector<int32_t> chk{0}, che{0}, chc{0}, src;
+  std::vector<uint16_t> dst, cpos, cid, est((size_t)nnz);
+  std::vector<double> cval;
+  std::unordered_map<uint64_t, uint16_t> cmap;
+  std::vector<std::pair<int32_t, int32_t>> gat;
+  for (int64_t k = 0; k < nnz;) {
+    int64_t k1 = k + 1, tot = stage_len[k];
+    while (k1 < nnz && k1 - k < EXA_CMP_CAP && tot + stage_len[k1] <= EXA_CMP_CAP) tot += stage_len[k1++];
+    if (tot > EXA_CMP_CAP) {  // one long entry: every non-dropped slot gathered, slot order
+      for (int64_t e = ptr[k]; e < ptr[k + 1]; ++e)
+        if (cls(ent[e]) != 1) src.push_back(ent[e]), dst.push_back(0);
+      est[k] = 0;
+    } else {
+      gat.clear();
+      int32_t pos = 0;
+      for (int64_t q = k; q < k1; ++q) {
+        est[q] = (uint16_t)pos;
+        for (int64_t e = ptr[q]; e < ptr[q + 1]; ++e) {
+          const int c = cls(ent[e]);
+          if (c == 1) continue;
+          uint16_t id = 0;
+          bool as_const = false;
+          if (c == 2) {
+            uint64_t bits;
+            std::memcpy(&bits, known_val + ent[e], 8);
+            auto it = cmap.find(bits);
+            if (it != cmap.end()) {
+              id = it->second;
+              as_const = true;
+            } else if (cval.size() < 65535) {
+              id = (uint16_t)cval.size();
+              cmap.emplace(bits, id);
+              cval.push_back(known_val[ent[e]]);
+              as_const = true;
+            }
+          }
+          if (as_const) {
+            cpos.push_back((uint16_t)pos);
+            cid.push_back(id);
+          } else {
+            gat.emplace_back(ent[e], pos);
+          }
+          ++pos;
+        }
+      }
+      std::sort(gat.begin(), gat.end());
+      for (auto& g : gat) src.push_back(g.first), dst.push_back((uint16_t)g.second);
+    }
+    chk.push_back((int32_t)k1);
+    che.push_back((int32_t)src.size());
+    chc.push_back((int32_t)cpos.size());
+    k = k1;
+  }
   DeviceGuard g(p->device);
   ExaPattern* q = new ExaPattern();
   q->device = p->device;
   q->n_raw = n_raw;
   q->nnz = nnz;
-  int rc = dev_upload(&q->ptr, ptr, (size_t)(nnz + 1));
-  if (!rc) rc = dev_upload(&q->ent, ent, (size_t)n_raw);
+  q->nch = (int32_t)(chk.size() - 1);
+  q->ipt = ipt;
+  int rc = dev_upload(&q->chk, chk.data(), chk.size());
+  if (!rc) rc = dev_upload(&q->che, che.data(), che.size());
+  if (!rc) rc = dev_upload(&q->chc, chc.data(), chc.size());
+  if (!rc) rc = dev_upload(&q->src, src.data(), src.size());
+  if (!rc) rc = dev_upload(&q->dst, dst.data(), dst.size());
+  if (!rc) rc = dev_upload(&q->cpos, cpos.data(), cpos.size());
+  if (!rc) rc = dev_upload(&q->cid, cid.data(), cid.size());
+  if (!rc) rc = dev_upload(&q->est, est.data(), est.size());
+  if (!rc) rc = dev_upload(&q->cval, cval.data(), cval.size());
   if (rc) {
     exa_pattern_destroy(q);
     return rc;
@@ -1059,10 +1303,22 @@ int exa_pattern_create(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* pt
   return 0;
 }
 
+int exa_pattern_create(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
+                       ExaPattern** out) {
+  return exa_pattern_create_known(p, n_raw, nnz, ptr, ent, nullptr, nullptr, out);
+}
+
 void exa_pattern_destroy(ExaPattern* q) {
   if (!q) return;
-  cudaFree(q->ptr);
-  cudaFree(q->ent);
+  cudaFree(q->chk);
+  cudaFree(q->che);
+  cudaFree(q->chc);
+  cudaFree(q->src);
+  cudaFree(q->dst);
+  cudaFree(q->cpos);
+  cudaFree(q->cid);
+  cudaFree(q->est);
+  cudaFree(q->cval);
   delete q;
 }
 
@@ -1075,30 +1331,40 @@ static int set_compressed(ExaPlan* p, ExaWorkspace* w, const ExaPattern* jp, con
     return fail("exa_eval_set_compressed: pattern does not match the plan's raw J / H slots");
   if ((jp && jp->device != p->device) || (hp && hp->device != p->device))
     return fail("exa_eval_set_compressed: pattern on another device");
+  if (jp && hp && jp->ipt != hp->ipt) return fail("exa_eval_set_compressed: patterns chunked for different EXA_CMP_IPT");
   double* rawJ = jp ? w->dJ : jc;
   double* rawH = hp ? w->dH : hc;
   int rc = exa_eval_set(p, w, x, mult, w_obj, c, rawJ, rawH, st);
   if (rc) return rc;
-  const int64_t nJ = jp ? jp->nnz : 0, nH = hp ? hp->nnz : 0;
-  if (nJ + nH == 0) return 0;
-  const int64_t* ptrJ = jp ? jp->ptr : nullptr;
-  const int32_t* entJ = jp ? jp->ent : nullptr;
-  const int64_t* ptrH = hp ? hp->ptr : nullptr;
-  const int32_t* entH = hp ? hp->ent : nullptr;
-  const double* cJ = rawJ;
-  const double* cH = rawH;
-  void* args[] = {(void*)&nJ, (void*)&ptrJ, (void*)&entJ, (void*)&cJ, (void*)&jc,
-                  (void*)&nH, (void*)&ptrH, (void*)&entH, (void*)&cH, (void*)&hc};
+  const int nchJ = jp ? jp->nch : 0, nchH = hp ? hp->nch : 0;
+  if (nchJ + nchH == 0) return 0;
+  ExaCmpArgs aJ = {}, aH = {};
+  if (jp) aJ = ExaCmpArgs{jp->chk, jp->che, jp->chc, jp->src, jp->dst, jp->cpos, jp->cid, jp->est, jp->cval, rawJ, jc};
+  if (hp) aH = ExaCmpArgs{hp->chk, hp->che, hp->chc, hp->src, hp->dst, hp->cpos, hp->cid, hp->est, hp->cval, rawH, hc};
+  void* args[] = {(void*)&nchJ, (void*)&aJ, (void*)&aH};
+  const int ipt = jp ? jp->ipt : hp->ipt;
+  const void* fn = ipt == 4 ? (const void*)exa_compress2_kernel<4, 7>
+                 : ipt == 12 ? (const void*)exa_compress2_kernel<12, 4>
+                 : ipt == 16 ? (const void*)exa_compress2_kernel<16, 3>
+                             : (const void*)exa_compress2_kernel<8, 6>;
+  const size_t smem = (size_t)EXA_CMP_THREADS * ipt * 10 + 2;
+  if (smem > 48 * 1024) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert({p->device, fn}).second) CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid_for(nJ + nH, 256));
-  cfg.blockDim = dim3(256);
+  cfg.gridDim = dim3((unsigned)(nchJ + nchH));
+  cfg.blockDim = dim3(EXA_CMP_THREADS);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = p->pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CU(cudaLaunchKernelExC(&cfg, (const void*)exa_compress2_kernel, args));
+  CU(cudaLaunchKernelExC(&cfg, fn, args));
   return 0;
 }
 
@@ -1180,6 +1446,21 @@ int exa_eval_obj(ExaPlan* p, ExaWorkspace* ws, const double* x, double* out, exa
   A.V = w->V;
   int rc = launch_mode(p, w, EXA_MODE_OBJV, A, st);
   if (rc) return rc;
+  const size_t smem = obj_fused_smem(p->n_leaves, p->n_prog);
+  if (p->obj_leaf_max <= EXA_OBJ_LEAF_MAX && smem <= EXA_OBJ_FUSED_SMEM_MAX) {
+    if (smem > 48 * 1024) {  // opt in once per device
+      static std::mutex mu;
+      static bool done[64] = {};
+      std::lock_guard<std::mutex> lk(mu);
+      if (p->device < 64 && !done[p->device]) {
+        CU(cudaFuncSetAttribute(exa_obj_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, EXA_OBJ_FUSED_SMEM_MAX));
+        done[p->device] = true;
+      }
+    }
+    exa_obj_fused<<<1, EXA_OBJ_THREADS, smem, st>>>(w->V, p->leaves, p->n_leaves, p->prog, p->n_prog, out);
+    CU(cudaGetLastError());
+    return 0;
+  }
   if (p->n_leaves) {
     exa_obj_leaves<<<grid_for(p->n_leaves, 128), 128, 0, st>>>(w->V, p->leaves, p->n_leaves, w->leafsum);
     CU(cudaGetLastError());

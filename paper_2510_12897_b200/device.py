@@ -55,6 +55,8 @@ BUCKET_MAX_N = 48                      # at most this many distinct counts per b
 # many-wave sets (twice the threads hide more latency: MP96 39.4 vs 40.7 us)
 GROUP_MAX_ENV = os.environ.get("EXA_GROUP_MAX", "auto")
 ATTACH = os.environ.get("EXA_ATTACH", "1") == "1"  # light terms join heavy groups
+# instance-window CTA order of many-wave batched sets (0 = natural order)
+LOCALITY_W = int(os.environ.get("EXA_LOCALITY_W", "64"))
 GROUP_RPT = int(os.environ.get("EXA_GROUP_RPT", "1"))  # records per thread of term groups (ILP)
 ATTACH_AUGS = os.environ.get("EXA_ATTACH_AUGS", "1") == "1"  # groups write aligned augments' J/H
 HALF_ROWS = os.environ.get("EXA_HALF_ROWS", "1") == "1"  # long bucket rows of <= 15 entries: half a warp each
@@ -527,8 +529,51 @@ class HostLayout:
         # persistent kernels (specialised modules): PERSIST virtual CTAs per real CTA
         self.persist = [PERSIST if (self.specialised and self.n_ctas[kid]) else 0 for kid in range(_lib.NKERN)]
         self.pdl = PDL
+        # CTA dispatch order of the many-wave set kernel for batched models
+        # whose variables are (element, instance) element-major: CTAs sorted by
+        # the instance window their records gather from, so the x / y rows of
+        # one window stay in L2 while all of its terms and rows are evaluated
+        self.cta_perm_off = None
+        period = getattr(plan, "batch_period", None)
+        if (self.specialised and LOCALITY_W > 0 and period and period >= 2 * LOCALITY_W
+                and self.threads[1] > 32 and not any(self.persist)):
+            perm = self._locality_order(terms, int(period))
+            if perm is not None:
+                self.cta_perm_off = int(self.i32.size)
+                self.i32 = np.concatenate([self.i32, perm.astype(np.int32)])
         self.source = module_source(self.patterns, layout=self if self.specialised else None,
                                     threads=self.threads[1])
+
+    def _locality_order(self, terms, period: int):
+        """Real CTA -> virtual CTA of the set kernel (light half): virtual CTAs
+        sorted by (instance window of their first record, virtual index).  A
+        record's instance is the first gathered variable's index modulo the
+        model's ``batch_period`` (element-major batched layouts: variable
+        (i, k) at i * period + k); row buckets use their row's base term."""
+        kid = 2 * _lib.MODE_SET + 1
+        th = self.threads[1]
+        n = self.n_ctas[kid]
+        if n == 0:
+            return None
+        key = np.zeros(n, dtype=np.int64)
+        for (t, kind, cta0, nrec, rpt) in self.segs[kid]:
+            nc = (nrec + th * rpt - 1) // (th * rpt)
+            r0 = np.arange(nc, dtype=np.int64) * th * rpt
+            col = None
+            if kind == SEG_GROUP:
+                u = self.groups[t][1][0]
+                col = np.asarray(terms[u].cols[0], dtype=np.int64)[r0]
+            elif kind == SEG_TERM and terms[t].tape.k:
+                col = np.asarray(terms[t].cols[0], dtype=np.int64)[r0]
+            elif (kind & 15) == SEG_BUCKET:
+                bk = self.buckets[t]["buckets"][kind >> 4]
+                q = r0 // (bk["d"] if bk["d"] >= 16 else 1)
+                rows = self.i32[bk["rows_off"]:bk["rows_off"] + bk["n"]].astype(np.int64)[np.minimum(q, bk["n"] - 1)]
+                col = (np.asarray(terms[t].cols[0], dtype=np.int64)[rows] if terms[t].tape.k else rows)
+            if col is None:
+                col = np.minimum(r0, nrec - 1)
+            key[cta0:cta0 + nc] = (col % period) // LOCALITY_W
+        return np.lexsort((np.arange(n), key))
 
     def _group_max(self, terms) -> int:
         if self.group_max_req is not None:

@@ -653,9 +653,12 @@ def _kernel_source(layout, m, half, kname) -> str:
                  f"    EXA_TRACE_END(b, tid, {threads});",
                  "  }"]
     else:
+        perm = getattr(layout, "cta_perm_off", None)
+        b0 = f"__ldg(A.i32 + {perm}LL + blockIdx.x)" if (perm is not None and kid == 1) else "(int)blockIdx.x"
         body += ["  EXA_TRACE_BEGIN();",
-                 f"  exa_vb_{kname}<@LDH@>((int)blockIdx.x, (int)threadIdx.x, A);",
-                 f"  EXA_TRACE_END((int)blockIdx.x, (int)threadIdx.x, {threads});"]
+                 f"  const int vb_ = {b0};",
+                 f"  exa_vb_{kname}<@LDH@>(vb_, (int)threadIdx.x, A);",
+                 f"  EXA_TRACE_END(vb_, (int)threadIdx.x, {threads});"]
     # release the dependent grid only when this CTA's work is issued (an early
     # release lets later grids' waiting CTAs take the slots this grid needs)
     body.append("  EXA_GRID_RELEASE();")

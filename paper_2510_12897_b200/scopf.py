@@ -213,7 +213,12 @@ def scopf_model(case, contingencies, form: str = "polar", corrective_ratio: floa
         v.pg["i1"] - v.pg["i0"],
         _keyed(DataTable({"i0": flat(li, np.zeros(li.size, dtype=np.int64)), "i1": flat(li, lkk)}), li, lkk, S),
         lb=-lim, ub=lim)
-    model = core.compile(lower_to_gpu=lower_to_gpu)
+    model = core.compile(lower_to_gpu=False)
+    # element-major (element, instance) layout: variable (i, k) at i * Sl + k;
+    # the device layout dispatches the set kernel's CTAs by instance window
+    model.plan.batch_period = Sl
+    if lower_to_gpu:
+        model.to_device()
     model.build_seconds = time.perf_counter() - t_start
     model.instances = local
     return model, v, c

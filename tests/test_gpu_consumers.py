@@ -41,6 +41,9 @@ def _ref():
     if str(REF) not in sys.path:
         sys.path.insert(0, str(REF))
     import simdnlp
+    import simdnlp.autodiff  # noqa: F401  - submodules the consumers resolve names in
+    import simdnlp.derivcheck  # noqa: F401
+    import simdnlp.solver  # noqa: F401
 
     return simdnlp
 

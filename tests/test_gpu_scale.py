@@ -153,3 +153,20 @@ def test_period_shards_on_gpu_reassemble_global():
         sc, sJ, sH = _gpu_set(sh.model, x[sh.var_map], y[sh.row_map], w)
         c[sh.row_map], J[sh.jac_map], H[sh.hess_map] = sc, sJ, sH
     assert ieee_equal(c, gc) and ieee_equal(J, gJ) and ieee_equal(H, gH)
+
+
+@pytest.mark.parametrize("name", ["case13659", "mp96_case1354"])
+def test_compressed_set_at_scale(name):
+    """eval_callback_set_compressed at BASELINE sizes: the chunked segmented
+    sum (known constants folded from the pattern, +0.0 slots skipped) is bit
+    for bit np.bincount of the same plan's raw slots, for both patterns."""
+    from paper_2510_12897_b200 import eval_callback_set_compressed, model_patterns
+
+    model, (x, y, w) = workload(name)
+    c, J, H = _gpu_set(model, x, y, w)
+    jp, hp = model_patterns(model)
+    cc, Jc, Hc = np.empty(model.ncon), np.empty(jp.nnz), np.empty(hp.nnz)
+    eval_callback_set_compressed(model, x, y, w, cc, Jc, Hc)
+    assert np.array_equal(cc.view(np.int64), c.view(np.int64))
+    assert np.array_equal(Jc.view(np.int64), O.sum_values(jp.slot_map, jp.nnz, J).view(np.int64))
+    assert np.array_equal(Hc.view(np.int64), O.sum_values(hp.slot_map, hp.nnz, H).view(np.int64))
