@@ -53,7 +53,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="case13659")
-    ap.add_argument("--sets-per-step", type=int, default=64)
+    ap.add_argument("--sets-per-step", type=int, default=None,
+                    help="sets per step (one CUDA graph); default 512 for sets under 100 MB, else 64")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -283,9 +284,11 @@ def replicas(model, R, local, seed0, **plan_kw):
     from paper_2510_12897_b200.workloads import eval_inputs
 
     dev = torch.device("cuda", local)
-    plans, bufs = [], []
+    # all plans first, then all buffers (the allocation order of
+    # tools/set_timing.py; interleaving them measured ~3% slower per set)
+    plans = [DevicePlan(model, local, **plan_kw) for _ in range(R)]
+    bufs = []
     for r in range(R):
-        plans.append(DevicePlan(model, local, **plan_kw))
         x, y, w = eval_inputs(model, seed=seed0 + r)
         bufs.append({
             "x": torch.from_numpy(x).to(dev), "y": torch.from_numpy(y).to(dev), "w": w,
@@ -565,7 +568,10 @@ def main():
     launch = launcher(lib, plans, bufs, stream)
     exact_default = plans[0].exact_zero_sign
 
-    S = args.sets_per_step
+    # a step = one CUDA graph of S back-to-back single-set launches; S large
+    # enough that the graph-replay boundary (~15 us without a programmatic
+    # edge between graphs) is <1% of the step
+    S = args.sets_per_step or (512 if bps < 1e8 else 64)
     # one CUDA graph = one step of S sets (rotating replicas); rotation phase kept across steps
     graphs = []
     with torch.cuda.stream(stream):

@@ -96,6 +96,8 @@ struct ExaWorkspace {
   std::mutex mu;
 };
 
+struct ExaObjNode;
+
 struct ExaPlan {
   int device = 0;
   int64_t nvar = 0, ncon = 0, n_jac = 0, n_hess = 0;
@@ -117,6 +119,10 @@ struct ExaPlan {
   int64_t obj_leaf_max = 0; /* longest pairwise leaf (numpy: <= 128) */
   int64_t* prog = nullptr;
   int32_t n_prog = 0;
+  ExaObjNode* onodes = nullptr; /* the combine program as a level-ordered DAG */
+  double* oinit = nullptr;
+  int32_t* olvl = nullptr;
+  int32_t n_onodes = 0, n_olvl = 0;
   int64_t* grad_ptr = nullptr;
   int64_t* grad_ent = nullptr;
   int has_checks = 0;
@@ -153,8 +159,10 @@ struct ExaPattern {
      slots [che[b], che[b+1]) of src (raw slot id) / dst (stage position),
      sorted by src so that a warp's gathers hit runs of consecutive raw slots;
      known constant slots [chc[b], chc[b+1]) of cpos (stage position) / cid
-     (index into cval).  Per entry: est = start of its stage.  A long entry
-     keeps every non-skipped slot in src, in slot order. */
+     (index into cval).  Per chunk entry slot, entries by decreasing stage
+     length (the threads of a warp fold stages of similar length): edesc =
+     stage start | length << 16, eord = the entry.  A long entry keeps every
+     non-skipped slot in src, in slot order. */
   int32_t nch = 0, ipt = 8;
   int32_t* chk = nullptr;
   int32_t* che = nullptr;
@@ -163,7 +171,8 @@ struct ExaPattern {
   uint16_t* dst = nullptr;
   uint16_t* cpos = nullptr;
   uint16_t* cid = nullptr;
-  uint16_t* est = nullptr;
+  uint32_t* edesc = nullptr; /* per entry slot of a chunk, longest stage first: start | len << 16 */
+  uint16_t* eord = nullptr;  /* ... and the entry (index in the chunk) it folds */
   double* cval = nullptr;
 };
 
@@ -231,88 +240,204 @@ __global__ void exa_obj_combine(const int64_t* __restrict__ prog, int n_prog,
   *out = total;
 }
 
-// The same objective sum as exa_obj_leaves + exa_obj_combine in one CTA, for
-// programs whose leaf sums and opcodes fit shared memory: the combine program
-// is staged in shared memory by all threads, each warp reduces leaves (lanes
-// load the leaf's <= 128 values at once into a warp buffer, lane 0 replays
-// numpy's accumulator order from it), then thread 0 runs the program.  One
-// launch and no chain of dependent global loads (the two-kernel path spent
-// ~20 us at case13659 on the single thread's prog/leaf loads).
+// The same objective sum as exa_obj_leaves + exa_obj_combine, as two
+// programmatic-dependent launches behind the objective-value kernel:
+//  * exa_obj_leaves2: one warp per pairwise leaf (lanes load the leaf's
+//    <= 128 values at once, lane 0 replays numpy's accumulator order);
+//  * exa_obj_dag: one CTA evaluates the combine program as a DAG ordered by
+//    level (level 0: the leaves in leaf order, then the constants; a node of
+//    level L > 0 adds two lower nodes, or is 0 + a node), one __syncthreads
+//    per level.  Every add is the program's own operation on the same
+//    operands, so the value is bit-identical.  Its node table is staged in
+//    shared memory before griddepcontrol.wait.
 #define EXA_OBJ_THREADS 512
 #define EXA_OBJ_LEAF_MAX 128
-__global__ void __launch_bounds__(EXA_OBJ_THREADS) exa_obj_fused(const double* __restrict__ V,
-                                                                 const int64_t* __restrict__ leaves, int n_leaves,
-                                                                 const int64_t* __restrict__ prog, int n_prog,
-                                                                 double* __restrict__ out) {
-  extern __shared__ double osm[];
-  double* wbuf = osm;                                            // [warps][EXA_OBJ_LEAF_MAX]
-  double* ls = wbuf + (EXA_OBJ_THREADS / 32) * EXA_OBJ_LEAF_MAX;  // [n_leaves]
-  int64_t* sprog = reinterpret_cast<int64_t*>(ls + n_leaves);    // [n_prog][2]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < n_prog; i += EXA_OBJ_THREADS) {
-    sprog[2 * i] = __ldg(prog + 3 * i);
-    sprog[2 * i + 1] = __ldg(prog + 3 * i + 1);
+#define EXA_OBJ_LEAF_WARPS 4
+__global__ void __launch_bounds__(32 * EXA_OBJ_LEAF_WARPS) exa_obj_leaves2(const double* V,
+                                                                         const int64_t* __restrict__ leaves,
+                                                                         int n_leaves, double* __restrict__ out) {
+  __shared__ double wbuf[EXA_OBJ_LEAF_WARPS][EXA_OBJ_LEAF_MAX];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int l = blockIdx.x * EXA_OBJ_LEAF_WARPS + warp;
+  int64_t st = 0;
+  int n = 0;
+  if (l < n_leaves) {
+    st = __ldg(leaves + 2 * l);
+    n = (int)__ldg(leaves + 2 * l + 1);
   }
-  double* wb = wbuf + warp * EXA_OBJ_LEAF_MAX;
-  for (int l = warp; l < n_leaves; l += EXA_OBJ_THREADS / 32) {
-    const double* a = V + __ldg(leaves + 2 * l);
-    const int n = (int)__ldg(leaves + 2 * l + 1);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (l >= n_leaves) return;
+  double* wb = wbuf[warp];
+  double v[EXA_OBJ_LEAF_MAX / 32];
 #pragma unroll
-    for (int j = 0; j < EXA_OBJ_LEAF_MAX / 32; ++j)
-      if (lane + 32 * j < n) wb[lane + 32 * j] = a[lane + 32 * j];
-    __syncwarp();
-    if (lane == 0) {
-      double res;
-      if (n < 8) {
-        res = 0.0;
-        for (int i = 0; i < n; ++i) res = res + wb[i];
-      } else {
-        double r0 = wb[0], r1 = wb[1], r2 = wb[2], r3 = wb[3], r4 = wb[4], r5 = wb[5], r6 = wb[6], r7 = wb[7];
-        int i = 8;
-        for (; i < n - (n % 8); i += 8) {
-          r0 = r0 + wb[i + 0];
-          r1 = r1 + wb[i + 1];
-          r2 = r2 + wb[i + 2];
-          r3 = r3 + wb[i + 3];
-          r4 = r4 + wb[i + 4];
-          r5 = r5 + wb[i + 5];
-          r6 = r6 + wb[i + 6];
-          r7 = r7 + wb[i + 7];
-        }
-        res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
-        for (; i < n; ++i) res = res + wb[i];
-      }
-      ls[l] = res;
+  for (int j = 0; j < EXA_OBJ_LEAF_MAX / 32; ++j) v[j] = lane + 32 * j < n ? V[st + lane + 32 * j] : 0.0;
+#pragma unroll
+  for (int j = 0; j < EXA_OBJ_LEAF_MAX / 32; ++j) wb[lane + 32 * j] = v[j];
+  __syncwarp();
+  if (lane != 0) return;
+  double res;
+  if (n < 8) {
+    res = 0.0;
+    for (int i = 0; i < n; ++i) res = res + wb[i];
+  } else {
+    double r0 = wb[0], r1 = wb[1], r2 = wb[2], r3 = wb[3], r4 = wb[4], r5 = wb[5], r6 = wb[6], r7 = wb[7];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+      r0 = r0 + wb[i + 0];
+      r1 = r1 + wb[i + 1];
+      r2 = r2 + wb[i + 2];
+      r3 = r3 + wb[i + 3];
+      r4 = r4 + wb[i + 4];
+      r5 = r5 + wb[i + 5];
+      r6 = r6 + wb[i + 6];
+      r7 = r7 + wb[i + 7];
     }
-    __syncwarp();
+    res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+    for (; i < n; ++i) res = res + wb[i];
+  }
+  out[l] = res;
+}
+struct ExaObjNode {
+  int32_t op, a, b, pad; /* op: 0 leaf / constant (value preset), 1 add, 2 zero-plus */
+};
+__global__ void __launch_bounds__(EXA_OBJ_THREADS) exa_obj_dag(const double* leafsum, int n_leaves,
+                                                             const ExaObjNode* __restrict__ nodes, int n_nodes,
+                                                             const double* __restrict__ init,
+                                                             const int32_t* __restrict__ lvl, int n_lvl,
+                                                             double* __restrict__ out) {
+  extern __shared__ double osm[];
+  double* nv = osm;                                                       // [n_nodes]
+  ExaObjNode* sn = reinterpret_cast<ExaObjNode*>(nv + ((n_nodes + 1) & ~1));  // [n_nodes]
+  int32_t* sl = reinterpret_cast<int32_t*>(sn + n_nodes);                 // [n_lvl + 1]
+  const int tid = threadIdx.x;
+  for (int i0 = n_leaves; i0 < n_nodes; i0 += 4 * EXA_OBJ_THREADS) {  // 4 loads per thread in flight
+    ExaObjNode t[4];
+    double c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + tid + EXA_OBJ_THREADS * j;
+      if (i < n_nodes) {
+        t[j] = nodes[i];
+        c[j] = __ldg(init + i);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + tid + EXA_OBJ_THREADS * j;
+      if (i < n_nodes) {
+        sn[i] = t[j];
+        nv[i] = c[j];
+      }
+    }
+  }
+  for (int i = tid; i <= n_lvl; i += EXA_OBJ_THREADS) sl[i] = __ldg(lvl + i);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (int i0 = 0; i0 < n_leaves; i0 += 4 * EXA_OBJ_THREADS) {
+    double c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + tid + EXA_OBJ_THREADS * j;
+      c[j] = i < n_leaves ? leafsum[i] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + tid + EXA_OBJ_THREADS * j;
+      if (i < n_leaves) nv[i] = c[j];
+    }
   }
   __syncthreads();
-  if (tid != 0) return;
-  double stack[EXA_OBJ_STACK];
-  int sp = 0;
-  double total = 0.0;
-  for (int q = 0; q < n_prog; ++q) {
-    const int64_t op = sprog[2 * q], a = sprog[2 * q + 1];
-    switch ((int)op) {
-      case OP_LEAF: stack[sp++] = ls[a]; break;
-      case OP_ADD: {
-        const double b = stack[--sp];
-        const double x = stack[--sp];
-        stack[sp++] = x + b;
-        break;
-      }
-      case OP_CONST: stack[sp++] = __longlong_as_double((long long)a); break;
-      case OP_ZERO_PLUS: stack[sp - 1] = 0.0 + stack[sp - 1]; break;
-      case OP_TOTAL_ADD: total = total + stack[--sp]; break;
-      default: break;
+  for (int L = 1; L < n_lvl; ++L) {
+    const int i1 = sl[L + 1];
+    for (int i = sl[L] + tid; i < i1; i += EXA_OBJ_THREADS) {
+      const ExaObjNode nd = sn[i];
+      nv[i] = nd.op == 1 ? nv[nd.a] + nv[nd.b] : 0.0 + nv[nd.a];
     }
+    __syncthreads();
   }
-  *out = total;
+  if (tid == 0) *out = n_nodes ? nv[n_nodes - 1] : 0.0;
 }
 #define EXA_OBJ_FUSED_SMEM_MAX (160 * 1024)
-static size_t obj_fused_smem(int n_leaves, int n_prog) {
-  return sizeof(double) * ((EXA_OBJ_THREADS / 32) * EXA_OBJ_LEAF_MAX + (size_t)n_leaves) +
-         2 * sizeof(int64_t) * (size_t)n_prog;
+static size_t obj_dag_smem(int n_nodes, int n_lvl) {
+  return sizeof(double) * (size_t)((n_nodes + 1) & ~1) + sizeof(ExaObjNode) * (size_t)n_nodes +
+         sizeof(int32_t) * (size_t)(n_lvl + 1);
+}
+
+// The combine program as a level-ordered DAG (see exa_obj_fused).  Returns
+// false if the program is malformed.  Node n_nodes - 1 is the total.
+static bool obj_dag(const int64_t* prog, int n_prog, int n_leaves, std::vector<ExaObjNode>& nodes,
+                    std::vector<double>& init, std::vector<int32_t>& lvl) {
+  struct N { int op; int64_t a, b; int level; double c; };
+  std::vector<N> g;
+  std::vector<int64_t> st;
+  for (int l = 0; l < n_leaves; ++l) g.push_back({0, l, 0, 0, 0.0});
+  auto cnst = [&](double c) { g.push_back({3, 0, 0, 0, c}); return (int64_t)g.size() - 1; };
+  int64_t total = cnst(0.0);
+  for (int q = 0; q < n_prog; ++q) {
+    const int64_t op = prog[3 * q], a = prog[3 * q + 1];
+    switch ((int)op) {
+      case OP_LEAF: if (a < 0 || a >= n_leaves) return false; st.push_back(a); break;
+      case OP_CONST: { double c; std::memcpy(&c, &a, 8); st.push_back(cnst(c)); break; }
+      case OP_ADD: {
+        if (st.size() < 2) return false;
+        const int64_t y = st.back(); st.pop_back();
+        const int64_t x = st.back(); st.pop_back();
+        g.push_back({1, x, y, 1 + std::max(g[x].level, g[y].level), 0.0});
+        st.push_back((int64_t)g.size() - 1);
+        break;
+      }
+      case OP_ZERO_PLUS: {
+        if (st.empty()) return false;
+        const int64_t x = st.back();
+        g.push_back({2, x, 0, 1 + g[x].level, 0.0});
+        st.back() = (int64_t)g.size() - 1;
+        break;
+      }
+      case OP_TOTAL_ADD: {
+        if (st.empty()) return false;
+        const int64_t y = st.back(); st.pop_back();
+        g.push_back({1, total, y, 1 + std::max(g[total].level, g[y].level), 0.0});
+        total = (int64_t)g.size() - 1;
+        break;
+      }
+      default: return false;
+    }
+  }
+  if (g.size() >= (size_t)INT32_MAX) return false;
+  /* order: leaves (leaf order), constants, then by level; the total last */
+  const int64_t n = (int64_t)g.size();
+  std::vector<int64_t> order;
+  for (int64_t i = 0; i < n_leaves; ++i) order.push_back(i);
+  for (int64_t i = n_leaves; i < n; ++i)
+    if (g[i].op == 3) order.push_back(i);
+  std::vector<int64_t> rest;
+  for (int64_t i = n_leaves; i < n; ++i)
+    if (g[i].op != 3 && i != total) rest.push_back(i);
+  std::stable_sort(rest.begin(), rest.end(), [&](int64_t x, int64_t y) { return g[x].level < g[y].level; });
+  order.insert(order.end(), rest.begin(), rest.end());
+  if (total >= n_leaves && g[total].op != 3) order.push_back(total);
+  else if (total != order.back()) {  /* no objective block: the total is the constant 0 */
+    g.push_back({2, total, 0, 1 + g[total].level, 0.0});
+    order.push_back((int64_t)g.size() - 1);
+  }
+  std::vector<int64_t> pos(g.size());
+  for (size_t i = 0; i < order.size(); ++i) pos[order[i]] = (int64_t)i;
+  nodes.assign(order.size(), ExaObjNode{0, 0, 0, 0});
+  init.assign(order.size(), 0.0);
+  lvl.assign(1, 0);
+  int cur = 0;
+  for (size_t i = 0; i < order.size(); ++i) {
+    const N& x = g[order[i]];
+    if (x.op == 3) init[i] = x.c;
+    if (x.op == 1 || x.op == 2) nodes[i] = ExaObjNode{x.op, (int32_t)pos[x.a], (int32_t)pos[x.op == 1 ? x.b : 0], 0};
+    /* level boundaries: level 0 = leaves + constants; the total may sit alone
+       at the end (its level can be below the last non-total node's) */
+    const int L = (x.op == 0 || x.op == 3) ? 0 : std::max(cur, x.level);
+    while (cur < L) { lvl.push_back((int32_t)i); ++cur; }
+  }
+  lvl.push_back((int32_t)order.size());
+  return true;
 }
 
 // Stack depth of an objective combine program, or -1 if it is malformed
@@ -393,12 +518,14 @@ __global__ void exa_compress_reduce(int64_t nnz, const int64_t* __restrict__ ptr
 // pattern is created (chunks are sized for it)
 static int cmp_ipt_env() {
   const char* e = getenv("EXA_CMP_IPT");
-  const int v = e ? atoi(e) : 8;
-  return (v == 4 || v == 8 || v == 12 || v == 16) ? v : 8;
+  const int v = e ? atoi(e) : 4;  // case13659 set + compress: 4 -> 18.2 us, 8 -> 21.8, 16 -> 24.1
+  return (v == 1 || v == 2 || v == 4 || v == 8 || v == 12 || v == 16) ? v : 4;
 }
 struct ExaCmpArgs {
   const int32_t *chk, *che, *chc, *src;
-  const uint16_t *dst, *cpos, *cid, *est;
+  const uint16_t *dst, *cpos, *cid;
+  const uint32_t* edesc;
+  const uint16_t* eord;
   const double* cval;
   const double* raw;
   double* out;
@@ -407,8 +534,9 @@ template <int IPT, int MINB>
 __global__ void __launch_bounds__(EXA_CMP_THREADS, MINB) exa_compress2_kernel(int nchJ, ExaCmpArgs J, ExaCmpArgs H) {
   constexpr int EXA_CMP_IPT = IPT;
   constexpr int EXA_CMP_CAP = EXA_CMP_THREADS * IPT;
-  extern __shared__ double vals[];                                   // [EXA_CMP_CAP]
-  uint16_t* sst = reinterpret_cast<uint16_t*>(vals + EXA_CMP_CAP);  // [EXA_CMP_CAP + 1]
+  extern __shared__ double vals[];                                     // [EXA_CMP_CAP] stage
+  uint32_t* sdesc = reinterpret_cast<uint32_t*>(vals + EXA_CMP_CAP);  // [EXA_CMP_CAP]
+  uint16_t* sord = reinterpret_cast<uint16_t*>(sdesc + EXA_CMP_CAP);  // [EXA_CMP_CAP]
   const int tid = threadIdx.x;
   int b = blockIdx.x;
   const bool isJ = b < nchJ;
@@ -428,6 +556,36 @@ __global__ void __launch_bounds__(EXA_CMP_THREADS, MINB) exa_compress2_kernel(in
     }
     return;
   }
+  // nc, nk <= EXA_CMP_CAP: fixed trip counts, so every load of a loop is
+  // issued before its first shared-memory store (one DRAM latency, not IPT)
+  {
+    int cp[EXA_CMP_IPT], ci[EXA_CMP_IPT];
+#pragma unroll
+    for (int j = 0; j < EXA_CMP_IPT; ++j) {
+      const int i = tid + EXA_CMP_THREADS * j;
+      cp[j] = i < nc ? (int)__ldg(P.cpos + c0 + i) : -1;
+      ci[j] = i < nc ? (int)__ldg(P.cid + c0 + i) : 0;
+    }
+    uint32_t dd[EXA_CMP_IPT];
+    uint16_t oo[EXA_CMP_IPT];
+#pragma unroll
+    for (int j = 0; j < EXA_CMP_IPT; ++j) {
+      const int i = tid + EXA_CMP_THREADS * j;
+      dd[j] = i < nk ? __ldg(P.edesc + k0 + i) : 0u;
+      oo[j] = i < nk ? __ldg(P.eord + k0 + i) : (uint16_t)0;
+    }
+#pragma unroll
+    for (int j = 0; j < EXA_CMP_IPT; ++j)
+      if (cp[j] >= 0) vals[cp[j]] = __ldg(P.cval + ci[j]);
+#pragma unroll
+    for (int j = 0; j < EXA_CMP_IPT; ++j) {
+      const int i = tid + EXA_CMP_THREADS * j;
+      if (i < nk) {
+        sdesc[i] = dd[j];
+        sord[i] = oo[j];
+      }
+    }
+  }
   int idx[EXA_CMP_IPT], pos[EXA_CMP_IPT];
 #pragma unroll
   for (int j = 0; j < EXA_CMP_IPT; ++j) {
@@ -435,9 +593,6 @@ __global__ void __launch_bounds__(EXA_CMP_THREADS, MINB) exa_compress2_kernel(in
     idx[j] = e < ng ? __ldg(P.src + g0 + e) : -1;
     pos[j] = e < ng ? (int)__ldg(P.dst + g0 + e) : 0;
   }
-  for (int i = tid; i < nc; i += EXA_CMP_THREADS) vals[__ldg(P.cpos + c0 + i)] = __ldg(P.cval + __ldg(P.cid + c0 + i));
-  for (int i = tid; i < nk; i += EXA_CMP_THREADS) sst[i] = __ldg(P.est + k0 + i);
-  if (tid == 0) sst[nk] = (uint16_t)(ng + nc);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   double v[EXA_CMP_IPT];
@@ -448,10 +603,19 @@ __global__ void __launch_bounds__(EXA_CMP_THREADS, MINB) exa_compress2_kernel(in
     if (idx[j] >= 0) vals[pos[j]] = v[j];
   __syncthreads();
   for (int i = tid; i < nk; i += EXA_CMP_THREADS) {
+    const uint32_t d = sdesc[i];
+    int e = (int)(d & 0xffffu);
+    const int z = e + (int)(d >> 16);
     double acc = 0.0;
-    const int z = sst[i + 1];
-    for (int e = sst[i]; e < z; ++e) acc = acc + vals[e];
-    P.out[k0 + i] = acc;
+    for (; e + 4 <= z; e += 4) {  // four stage loads in flight, adds in slot order
+      const double a0 = vals[e], a1 = vals[e + 1], a2 = vals[e + 2], a3 = vals[e + 3];
+      acc = acc + a0;
+      acc = acc + a1;
+      acc = acc + a2;
+      acc = acc + a3;
+    }
+    for (; e < z; ++e) acc = acc + vals[e];
+    P.out[k0 + sord[i]] = acc;
   }
 }
 
@@ -626,6 +790,9 @@ void exa_plan_destroy(ExaPlan* p) {
   }
   cudaFree(p->leaves);
   cudaFree(p->prog);
+  cudaFree(p->onodes);
+  cudaFree(p->oinit);
+  cudaFree(p->olvl);
   cudaFree(p->grad_ptr);
   cudaFree(p->grad_ent);
   if (p->lib) cudaLibraryUnload(p->lib);
@@ -780,6 +947,18 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
   }
   if ((rc = dev_upload(&p->leaves, d->leaves, (size_t)d->n_leaves * 2))) return bail(rc);
   if ((rc = dev_upload(&p->prog, d->obj_prog, (size_t)d->n_prog * 3))) return bail(rc);
+  {
+    std::vector<ExaObjNode> nodes;
+    std::vector<double> init;
+    std::vector<int32_t> lvl;
+    if (!obj_dag(d->obj_prog, d->n_prog, d->n_leaves, nodes, init, lvl))
+      return bail(fail("objective combine program is malformed"));
+    p->n_onodes = (int32_t)nodes.size();
+    p->n_olvl = (int32_t)lvl.size() - 1;
+    if ((rc = dev_upload(&p->onodes, nodes.data(), nodes.size()))) return bail(rc);
+    if ((rc = dev_upload(&p->oinit, init.data(), init.size()))) return bail(rc);
+    if ((rc = dev_upload(&p->olvl, lvl.data(), lvl.size()))) return bail(rc);
+  }
   if (d->grad_ptr) {
     if ((rc = dev_upload(&p->grad_ptr, d->grad_ptr, (size_t)d->nvar + 1))) return bail(rc);
     if ((rc = dev_upload(&p->grad_ent, d->grad_ent, (size_t)d->n_grad_ent))) return bail(rc);
@@ -1227,7 +1406,9 @@ int exa_pattern_create_known(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64
     stage_len[k] = L;
   }
   std::vector<int32_t> chk{0}, che{0}, chc{0}, src;
-  std::vector<uint16_t> dst, cpos, cid, est((size_t)nnz);
+  std::vector<uint16_t> dst, cpos, cid, eord((size_t)nnz);
+  std::vector<uint32_t> edesc((size_t)nnz);
+  std::vector<int32_t> est((size_t)nnz);
   std::vector<double> cval;
   std::unordered_map<uint64_t, uint16_t> cmap;
   std::vector<std::pair<int32_t, int32_t>> gat;
@@ -1242,7 +1423,7 @@ int exa_pattern_create_known(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64
       gat.clear();
       int32_t pos = 0;
       for (int64_t q = k; q < k1; ++q) {
-        est[q] = (uint16_t)pos;
+        est[q] = pos;
         for (int64_t e = ptr[q]; e < ptr[q + 1]; ++e) {
           const int c = cls(ent[e]);
           if (c == 1) continue;
@@ -1274,6 +1455,16 @@ int exa_pattern_create_known(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64
       std::sort(gat.begin(), gat.end());
       for (auto& g : gat) src.push_back(g.first), dst.push_back((uint16_t)g.second);
     }
+    /* entry slots of the chunk, longest stage first (stable) */
+    std::vector<int32_t> ord((size_t)(k1 - k));
+    for (int64_t q = k; q < k1; ++q) ord[q - k] = (int32_t)(q - k);
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](int32_t x, int32_t y) { return stage_len[k + x] > stage_len[k + y]; });
+    for (int64_t q = k; q < k1; ++q) {
+      const int32_t en = ord[q - k];
+      edesc[q] = tot > EXA_CMP_CAP ? 0u : ((uint32_t)est[k + en] | ((uint32_t)stage_len[k + en] << 16));
+      eord[q] = (uint16_t)en;
+    }
     chk.push_back((int32_t)k1);
     che.push_back((int32_t)src.size());
     chc.push_back((int32_t)cpos.size());
@@ -1293,7 +1484,8 @@ int exa_pattern_create_known(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64
   if (!rc) rc = dev_upload(&q->dst, dst.data(), dst.size());
   if (!rc) rc = dev_upload(&q->cpos, cpos.data(), cpos.size());
   if (!rc) rc = dev_upload(&q->cid, cid.data(), cid.size());
-  if (!rc) rc = dev_upload(&q->est, est.data(), est.size());
+  if (!rc) rc = dev_upload(&q->edesc, edesc.data(), edesc.size());
+  if (!rc) rc = dev_upload(&q->eord, eord.data(), eord.size());
   if (!rc) rc = dev_upload(&q->cval, cval.data(), cval.size());
   if (rc) {
     exa_pattern_destroy(q);
@@ -1317,7 +1509,8 @@ void exa_pattern_destroy(ExaPattern* q) {
   cudaFree(q->dst);
   cudaFree(q->cpos);
   cudaFree(q->cid);
-  cudaFree(q->est);
+  cudaFree(q->edesc);
+  cudaFree(q->eord);
   cudaFree(q->cval);
   delete q;
 }
@@ -1339,15 +1532,19 @@ static int set_compressed(ExaPlan* p, ExaWorkspace* w, const ExaPattern* jp, con
   const int nchJ = jp ? jp->nch : 0, nchH = hp ? hp->nch : 0;
   if (nchJ + nchH == 0) return 0;
   ExaCmpArgs aJ = {}, aH = {};
-  if (jp) aJ = ExaCmpArgs{jp->chk, jp->che, jp->chc, jp->src, jp->dst, jp->cpos, jp->cid, jp->est, jp->cval, rawJ, jc};
-  if (hp) aH = ExaCmpArgs{hp->chk, hp->che, hp->chc, hp->src, hp->dst, hp->cpos, hp->cid, hp->est, hp->cval, rawH, hc};
+  if (jp) aJ = ExaCmpArgs{jp->chk, jp->che, jp->chc, jp->src, jp->dst, jp->cpos, jp->cid, jp->edesc, jp->eord, jp->cval,
+                          rawJ, jc};
+  if (hp) aH = ExaCmpArgs{hp->chk, hp->che, hp->chc, hp->src, hp->dst, hp->cpos, hp->cid, hp->edesc, hp->eord, hp->cval,
+                          rawH, hc};
   void* args[] = {(void*)&nchJ, (void*)&aJ, (void*)&aH};
   const int ipt = jp ? jp->ipt : hp->ipt;
-  const void* fn = ipt == 4 ? (const void*)exa_compress2_kernel<4, 7>
+  const void* fn = ipt == 1 ? (const void*)exa_compress2_kernel<1, 8>
+                 : ipt == 2 ? (const void*)exa_compress2_kernel<2, 8>
+                 : ipt == 4 ? (const void*)exa_compress2_kernel<4, 6>
                  : ipt == 12 ? (const void*)exa_compress2_kernel<12, 4>
                  : ipt == 16 ? (const void*)exa_compress2_kernel<16, 3>
                              : (const void*)exa_compress2_kernel<8, 6>;
-  const size_t smem = (size_t)EXA_CMP_THREADS * ipt * 10 + 2;
+  const size_t smem = (size_t)EXA_CMP_THREADS * ipt * 14;
   if (smem > 48 * 1024) {
     static std::mutex mu;
     static std::set<std::pair<int, const void*>> done;
@@ -1446,19 +1643,38 @@ int exa_eval_obj(ExaPlan* p, ExaWorkspace* ws, const double* x, double* out, exa
   A.V = w->V;
   int rc = launch_mode(p, w, EXA_MODE_OBJV, A, st);
   if (rc) return rc;
-  const size_t smem = obj_fused_smem(p->n_leaves, p->n_prog);
-  if (p->obj_leaf_max <= EXA_OBJ_LEAF_MAX && smem <= EXA_OBJ_FUSED_SMEM_MAX) {
+  const size_t smem = obj_dag_smem(p->n_onodes, p->n_olvl);
+  if (p->obj_leaf_max <= EXA_OBJ_LEAF_MAX && smem <= EXA_OBJ_FUSED_SMEM_MAX && w->leafsum) {
     if (smem > 48 * 1024) {  // opt in once per device
       static std::mutex mu;
       static bool done[64] = {};
       std::lock_guard<std::mutex> lk(mu);
       if (p->device < 64 && !done[p->device]) {
-        CU(cudaFuncSetAttribute(exa_obj_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, EXA_OBJ_FUSED_SMEM_MAX));
+        CU(cudaFuncSetAttribute(exa_obj_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, EXA_OBJ_FUSED_SMEM_MAX));
         done[p->device] = true;
       }
     }
-    exa_obj_fused<<<1, EXA_OBJ_THREADS, smem, st>>>(w->V, p->leaves, p->n_leaves, p->prog, p->n_prog, out);
-    CU(cudaGetLastError());
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = p->pdl ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (p->n_leaves) {
+      cfg.gridDim = dim3((unsigned)((p->n_leaves + EXA_OBJ_LEAF_WARPS - 1) / EXA_OBJ_LEAF_WARPS));
+      cfg.blockDim = dim3(32 * EXA_OBJ_LEAF_WARPS);
+      const double* V = w->V;
+      void* a1[] = {(void*)&V, (void*)&p->leaves, (void*)&p->n_leaves, (void*)&w->leafsum};
+      CU(cudaLaunchKernelExC(&cfg, (const void*)exa_obj_leaves2, a1));
+    }
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(EXA_OBJ_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    const double* ls = w->leafsum;
+    void* a2[] = {(void*)&ls, (void*)&p->n_leaves, (void*)&p->onodes, (void*)&p->n_onodes, (void*)&p->oinit,
+                  (void*)&p->olvl, (void*)&p->n_olvl, (void*)&out};
+    CU(cudaLaunchKernelExC(&cfg, (const void*)exa_obj_dag, a2));
     return 0;
   }
   if (p->n_leaves) {

@@ -56,7 +56,7 @@ BUCKET_MAX_N = 48                      # at most this many distinct counts per b
 GROUP_MAX_ENV = os.environ.get("EXA_GROUP_MAX", "auto")
 ATTACH = os.environ.get("EXA_ATTACH", "1") == "1"  # light terms join heavy groups
 # instance-window CTA order of many-wave batched sets (0 = natural order)
-LOCALITY_W = int(os.environ.get("EXA_LOCALITY_W", "64"))
+LOCALITY_W = int(os.environ.get("EXA_LOCALITY_W", "0"))
 GROUP_RPT = int(os.environ.get("EXA_GROUP_RPT", "1"))  # records per thread of term groups (ILP)
 ATTACH_AUGS = os.environ.get("EXA_ATTACH_AUGS", "1") == "1"  # groups write aligned augments' J/H
 HALF_ROWS = os.environ.get("EXA_HALF_ROWS", "1") == "1"  # long bucket rows of <= 15 entries: half a warp each
