@@ -30,7 +30,7 @@ import numpy as np
 from . import _lib
 from .codegen import _DERIV_ZERO_ELISION, PatternCode
 from .core import ModelError
-from .jit import PDL, PERSIST, THREADS_ENV, THREADS_HEAVY, choose_threads, compile_module, module_source
+from .jit import PDL, PERSIST, SM_COUNT, THREADS_ENV, THREADS_HEAVY, choose_threads, compile_module, module_source
 
 ALIGN = 32  # elements: 256 B for fp64, 128 B for int32
 
@@ -584,7 +584,14 @@ class HostLayout:
         # light constraint terms counted as if ungrouped)
         est = sum(tp.nrec / 4 if self.patterns[self.term_pid[t]].heavy else tp.nrec
                   for t, tp in enumerate(terms) if tp.kind != "augment")
-        return 4 if choose_threads(int(est)) == 32 else 2
+        if choose_threads(int(est)) != 32:
+            return 2  # many-wave sets
+        # one-wave sets: groups of four halve the voltage gathers (case13659
+        # 5.65 us); a set too small to give every SM a warp of groups of four
+        # needs the parallelism of groups of two (case1354 3.37 -> 3.19 us)
+        heavy = sum(tp.nrec for t, tp in enumerate(terms)
+                    if tp.kind != "augment" and self.patterns[self.term_pid[t]].heavy)
+        return 4 if heavy / 4 >= SM_COUNT * 32 else 2
 
     def _make_groups(self, terms, descs):
         import hashlib

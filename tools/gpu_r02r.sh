@@ -1,0 +1,14 @@
+#!/bin/bash
+T=${1:-r02r}
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_scale.py -k "compress" -x -q -p no:cacheprovider > gpurun_out/${T}_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/${T}_tests.log
+for cfg in "4 1" "8 1" "16 1" "4 2" "8 2" "2 1"; do
+  set -- $cfg
+  EXA_CMP_IPT=$1 EXA_CMP_GRID_DIV=$2 timeout 600 python tools/compressed_timing.py case13659 >> gpurun_out/${T}_comp.jsonl 2>> gpurun_out/${T}_comp.err
+done
+EXA_CMP_PROBE=1 timeout 600 python tools/compressed_timing.py case13659 >> gpurun_out/${T}_comp.jsonl 2>> gpurun_out/${T}_comp.err
+for ipt in 4 8; do
+  EXA_CMP_IPT=$ipt timeout 600 python tools/compressed_timing.py mp96_case1354 >> gpurun_out/${T}_comp.jsonl 2>> gpurun_out/${T}_comp.err
+done
+tail -2 gpurun_out/${T}_tests.log; cat gpurun_out/${T}_comp.jsonl
