@@ -178,8 +178,9 @@ int exa_eval_set_batch(ExaPlan* plan, ExaWorkspace* ws, int64_t nsets, const dou
 /* exa_eval_set with HOST buffers (the reference-facing drop-in path: numpy
  * arrays in, numpy arrays out): copies x, mult to the workspace's device
  * staging, evaluates, copies c and the x-dependent J/H ranges back -- all
- * asynchronous on `stream` (synchronise it before reading the outputs; a
- * non-legacy stream gets one batched D2H call) -- and writes the plan's
+ * asynchronous on `stream` (synchronise it before reading the outputs;
+ * page-locked output arrays are written by one store kernel through their
+ * device mapping, EXA_D2H=dma selects copy-engine transfers) -- and writes the plan's
  * constant J/H runs (ExaPlanDesc.host_fill) into jac/hess with host threads
  * before returning.  Pinned host memory makes the copies asynchronous, so
  * sets on distinct workspaces and streams overlap their H2D copy, kernel and

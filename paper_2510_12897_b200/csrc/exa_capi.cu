@@ -99,6 +99,13 @@ struct ExaWorkspace {
 
 struct ExaObjNode;
 
+/* one CTA's share of the host path's D2H: output slots [a, e) of output arr */
+struct ExaD2HChunk {
+  int64_t a, e;
+  int32_t arr, pad;
+};
+constexpr int64_t kD2HChunk = 2048;  // doubles per CTA (16 KB)
+
 struct ExaPlan {
   int device = 0;
   int64_t nvar = 0, ncon = 0, n_jac = 0, n_hess = 0;
@@ -143,6 +150,18 @@ struct ExaPlan {
   std::vector<int32_t> wz_rows;
   /* ... and the complementary slot ranges copied D2H, (first, length) */
   std::vector<std::pair<int64_t, int64_t>> copy_jac, copy_hess;
+  /* the same ranges (c whole, then J, then H) cut into CTA chunks for the
+     device-to-host store kernel; chunks [d2h_c[k], d2h_c[k + 1]) belong to
+     output k (0 = c, 1 = J, 2 = H) */
+  struct ExaD2HChunk* d2h = nullptr;
+  int d2h_c[4] = {};
+  /* ... and as copy-engine operations: rows x [a, a + n) at pitch (slots) of
+     output arr; consecutive ranges of equal length and stride are one 2D copy
+     (a transfer costs the engine ~3.6 us on top of its bytes: 20 ranges of a
+     case13659 set run at 42 GB/s one by one, at the full 56 GB/s as rows of
+     one 2D copy -- tools/micro/d2hstore.cu) */
+  struct Op { int arr, rows; int64_t a, n, pitch; };
+  std::vector<Op> d2h_ops;
 };
 
 /* A compressed pattern (reference CompressedPattern, autodiff.py:660-674) on
@@ -820,6 +839,7 @@ void exa_plan_destroy(ExaPlan* p) {
   cudaFree(p->olvl);
   cudaFree(p->grad_ptr);
   cudaFree(p->grad_ent);
+  cudaFree(p->d2h);
   if (p->lib) cudaLibraryUnload(p->lib);
   delete p;
 }
@@ -896,6 +916,67 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
     }
     if ((rc = complement(sj, d->n_jac, p->copy_jac))) return bail(rc);
     if ((rc = complement(sh, d->n_hess, p->copy_hess))) return bail(rc);
+    // constant runs shorter than EXA_D2H_GAP slots between two copied ranges
+    // are copied with them instead of filled on the host (one transfer fewer)
+    const char* ge = std::getenv("EXA_D2H_GAP");
+    const int64_t gap = ge ? std::atoll(ge) : 0;
+    auto merge = [&](std::vector<std::pair<int64_t, int64_t>>& cp) {
+      std::vector<std::pair<int64_t, int64_t>> out;
+      for (auto& r : cp) {
+        if (!out.empty() && r.first - (out.back().first + out.back().second) <= gap)
+          out.back().second = r.first + r.second - out.back().first;
+        else
+          out.push_back(r);
+      }
+      cp.swap(out);
+    };
+    auto inside = [](const std::vector<std::pair<int64_t, int64_t>>& cp, int64_t a) {
+      auto it = std::upper_bound(cp.begin(), cp.end(), std::make_pair(a, INT64_MAX));
+      return it != cp.begin() && a < std::prev(it)->first + std::prev(it)->second;
+    };
+    if (gap > 0) {
+      merge(p->copy_jac);
+      merge(p->copy_hess);
+      auto drop = [&](auto& runs, const std::vector<std::pair<int64_t, int64_t>>& cp) {
+        runs.erase(std::remove_if(runs.begin(), runs.end(), [&](const auto& r) { return inside(cp, r.a); }), runs.end());
+      };
+      drop(p->fill_jac, p->copy_jac);
+      drop(p->fill_hess, p->copy_hess);
+      drop(p->fill_wz, p->copy_hess);
+    }
+    {
+      auto ops = [&](int arr, const std::vector<std::pair<int64_t, int64_t>>& cp) {
+        for (size_t i = 0; i < cp.size();) {
+          size_t j = i + 1;
+          const int64_t pitch = j < cp.size() ? cp[j].first - cp[i].first : 0;
+          while (j < cp.size() && cp[j].second == cp[i].second && cp[j].first - cp[j - 1].first == pitch) ++j;
+          p->d2h_ops.push_back({arr, (int)(j - i), cp[i].first, cp[i].second, j - i > 1 ? pitch : cp[i].second});
+          i = j;
+        }
+      };
+      std::vector<std::pair<int64_t, int64_t>> call;
+      if (d->ncon) call.push_back({0, d->ncon});
+      ops(0, call);
+      ops(1, p->copy_jac);
+      ops(2, p->copy_hess);
+    }
+    std::vector<ExaD2HChunk> ch;
+    auto cut = [&](int arr, const std::vector<std::pair<int64_t, int64_t>>& rs) {
+      p->d2h_c[arr] = (int)ch.size();
+      for (auto& r : rs)
+        for (int64_t o = 0; o < r.second; o += kD2HChunk)
+          ch.push_back({r.first + o, r.first + std::min(r.second, o + kD2HChunk), arr, 0});
+    };
+    std::vector<std::pair<int64_t, int64_t>> call;
+    if (d->ncon) call.push_back({0, d->ncon});
+    cut(0, call);
+    cut(1, p->copy_jac);
+    cut(2, p->copy_hess);
+    p->d2h_c[3] = (int)ch.size();
+    if (!ch.empty()) {
+      CU(cudaMalloc((void**)&p->d2h, ch.size() * sizeof(ExaD2HChunk)));
+      CU(cudaMemcpy(p->d2h, ch.data(), ch.size() * sizeof(ExaD2HChunk), cudaMemcpyHostToDevice));
+    }
   }
   p->threads[0] = d->threads[0] > 0 ? d->threads[0] : 128;
   p->threads[1] = d->threads[1] > 0 ? d->threads[1] : 256;
@@ -1262,6 +1343,44 @@ static bool pageable(const void* ptr) {
   return a.type == cudaMemoryTypeUnregistered;
 }
 
+// Host path, pinned outputs: the x-dependent output ranges stored by SMs
+// straight into the caller's page-locked arrays (mapped into the device's
+// address space), one launch for all ranges -- per-range DMA calls cost ~10 us
+// of CPU each.  One CTA per chunk; 16-byte accesses when source and
+// destination share their alignment.
+__global__ void __launch_bounds__(128) exa_d2h_store(const ExaD2HChunk* __restrict__ ch, int c0, double* d0, double* d1,
+                                                     double* d2, const double* s0, const double* s1, const double* s2) {
+  const ExaD2HChunk q = ch[c0 + blockIdx.x];
+  double* dst = q.arr == 0 ? d0 : (q.arr == 1 ? d1 : d2);
+  const double* src = q.arr == 0 ? s0 : (q.arr == 1 ? s1 : s2);
+  int64_t a = q.a;
+  const int64_t e = q.e;
+  if (((reinterpret_cast<uintptr_t>(dst) ^ reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    if (reinterpret_cast<uintptr_t>(dst + a) & 15) {
+      if (threadIdx.x == 0) dst[a] = __ldcs(src + a);
+      ++a;
+    }
+    const int64_t nv = (e - a) >> 1;
+    double2* dv = reinterpret_cast<double2*>(dst + a);
+    const double2* sv = reinterpret_cast<const double2*>(src + a);
+    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) dv[i] = __ldcs(sv + i);
+    if (((e - a) & 1) && threadIdx.x == 0) dst[e - 1] = __ldcs(src + e - 1);
+  } else {
+    for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) dst[i] = __ldcs(src + i);
+  }
+}
+
+// device address of a page-locked host array, or null (pageable / not mapped)
+static double* mapped(void* h) {
+  if (!h) return nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? static_cast<double*>(a.devicePointer) : nullptr;
+}
+
 // D2H ranges (dst host, src device, doubles) of one host-path set
 struct Range { double* dst; const double* src; int64_t n; };
 
@@ -1360,25 +1479,34 @@ static int host_eval(ExaPlan* p, ExaWorkspace* ws, int mode, const double* x, co
       }
     }
   } else {
-    // pinned outputs: D2H of everything but the constant runs (one batched
-    // call on a real stream); the constant runs are written meanwhile
-    std::vector<void*> dst, src;
-    std::vector<size_t> len;
-    for (const Range& r : d2h_ranges(p, w, c, jac, hess)) {
-      dst.push_back(r.dst);
-      src.push_back((void*)r.src);
-      len.push_back(r.n * sizeof(double));
-    }
-    if (!dst.empty()) {
-      if (st != nullptr && st != cudaStreamLegacy && st != cudaStreamPerThread) {
-        cudaMemcpyAttributes at = {};
-        at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-        size_t ai = 0, fidx = 0;
-        CU(cudaMemcpyBatchAsync(dst.data(), src.data(), len.data(), dst.size(), &at, &ai, 1, &fidx, st));
-      } else {
-        for (size_t i = 0; i < dst.size(); ++i)
-          CU(cudaMemcpyAsync(dst[i], src[i], len[i], cudaMemcpyDeviceToHost, st));
+    // pinned outputs: everything but the constant runs crosses PCIe while
+    // the constant runs are written on the host.  Default: one store kernel
+    // into the mapped arrays (case13659 e2e 4.09k sets/s); EXA_D2H=dma, or
+    // arrays not mapped: copy-engine transfers, 2D where ranges repeat at a
+    // constant stride (3.54k: every transfer adds ~3.6 us of engine time)
+    static const bool dma = [] { const char* e = std::getenv("EXA_D2H"); return e && std::strcmp(e, "dma") == 0; }();
+    double *mc = dma ? nullptr : mapped(c), *mj = dma ? nullptr : mapped(jac), *mh = dma ? nullptr : mapped(hess);
+    // the wanted outputs must be consecutive in chunk order (c, J, H)
+    const bool want[3] = {c != nullptr, jac != nullptr, hess != nullptr}, got[3] = {mc != nullptr, mj != nullptr, mh != nullptr};
+    int k0 = 0, k1 = 3;
+    while (k0 < 3 && !want[k0]) ++k0;
+    while (k1 > k0 && !want[k1 - 1]) --k1;
+    bool ok = !dma;
+    for (int k = k0; k < k1; ++k) ok = ok && want[k] && got[k];
+    const int c0 = p->d2h_c[k0 < 3 ? k0 : 3], n_ch = p->d2h_c[k1 > k0 ? k1 : k0 < 3 ? k0 : 3] - c0;
+    if (ok && n_ch > 0) {
+      exa_d2h_store<<<n_ch, 128, 0, st>>>(p->d2h, c0, mc, mj, mh, w->dc, w->dJ, w->dH);
+      CU(cudaGetLastError());
+    } else {
+      double* dst[3] = {c, jac, hess};
+      const double* src[3] = {w->dc, w->dJ, w->dH};
+      for (const ExaPlan::Op& o : p->d2h_ops) {
+        if (!dst[o.arr]) continue;
+        if (o.rows == 1)
+          CU(cudaMemcpyAsync(dst[o.arr] + o.a, src[o.arr] + o.a, o.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        else
+          CU(cudaMemcpy2DAsync(dst[o.arr] + o.a, o.pitch * sizeof(double), src[o.arr] + o.a, o.pitch * sizeof(double),
+                               o.n * sizeof(double), o.rows, cudaMemcpyDeviceToHost, st));
       }
     }
   }
