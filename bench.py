@@ -792,7 +792,9 @@ def main():
     assert np.array_equal(Hp_, Hn) and np.array_equal(Jp_, Jn)
     # the host path's H equals the device path's bit for bit (host-filled runs included)
     assert np.array_equal(slots[0]["H"].numpy().view(np.uint64), slots[1]["H"].numpy().view(np.uint64))
-    # latency view: one set at a time, synchronised per set
+    # latency view: one set at a time, synchronised per set (a synchronous
+    # caller's workspace: the call itself waits and writes the host mirrors)
+    _lib.check(lib.exa_workspace_set_flags(slots[0]["ws"], _lib.WS_SYNC_HOST), "workspace flags")
     t0 = time.perf_counter()
     for i in range(n_e2e // NS):
         e2e_issue(0)
@@ -812,7 +814,10 @@ def main():
     lay0 = plans[0].layout
     filled = 8 * int(lay0.fill_jac[:, 1].sum() + (lay0.fill_hess[:, 1].sum() if len(lay0.fill_hess) else 0)
                      + (lay0.fill_wzero[:, 1].sum() if len(lay0.fill_wzero) else 0))
-    d2h = 8 * (model.ncon + model.plan.n_jac_slots + model.plan.n_hess_slots) - filled
+    # ... and the mirror runs (exact +-copies of a copied run) are written by
+    # host threads from the arrived source, also inside the call
+    mirrored = 8 * int(sum(int(m[:, 1].sum()) for m in (lay0.mirror_jac, lay0.mirror_hess) if len(m)))
+    d2h = 8 * (model.ncon + model.plan.n_jac_slots + model.plan.n_hess_slots) - filled - mirrored
 
     if rank != 0:
         if ws > 1:
@@ -848,8 +853,10 @@ def main():
         "e2e": {"value": e2e_value, "unit": "sets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": (f"exa_eval_set_host (C ABI): pinned host x,y -> HBM -> set kernel -> pinned host c,J,H; "
                          f"one set per step, {NS} streams in round robin; constant / weighted-zero J/H runs "
-                         f"({filled / 1e6:.1f} MB) written by host threads, not copied"),
+                         f"({filled / 1e6:.1f} MB) and exact +-copies of copied runs ({mirrored / 1e6:.1f} MB) "
+                         f"written by host threads, not copied; D2H by one store kernel into the mapped arrays"),
                 "host_filled_bytes_per_step": filled,
+                "host_mirrored_bytes_per_step": mirrored,
                 "d2h_GBps": d2h * e2e_value / (1 if sharded else ws) / 1e9,
                 "sequential_value": e2e_seq, "numpy_api_value": e2e_numpy,
                 "numpy_api_pinned_value": e2e_numpy_pinned},

@@ -170,3 +170,63 @@ def test_compressed_set_at_scale(name):
     assert np.array_equal(cc.view(np.int64), c.view(np.int64))
     assert np.array_equal(Jc.view(np.int64), O.sum_values(jp.slot_map, jp.nnz, J).view(np.int64))
     assert np.array_equal(Hc.view(np.int64), O.sum_values(hp.slot_map, hp.nnz, H).view(np.int64))
+
+
+@pytest.mark.parametrize("name", ["case13659", "mp96_case1354"])
+@pytest.mark.parametrize("exact", [False, True])
+def test_host_path_bitwise_at_scale(name, exact):
+    """The host-buffer path at benchmark size: pinned outputs written by the
+    D2H store kernel, constant runs and host mirrors (exact +-copies) written
+    by host threads -- on NaN-initialised arrays, bit for bit the device
+    path's outputs, for the set and the single callbacks, in both zero-sign
+    modes; the pageable (numpy) form too."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2510_12897_b200 import _lib
+    from paper_2510_12897_b200.device import DevicePlan
+
+    model, (x, y, w) = workload(name)
+    dp = DevicePlan(model, 0, exact_zero_sign=exact)
+    # exact mode keeps the reference's 0 + x normalisations: fewer exact mirrors
+    assert len(dp.layout.mirror_hess) and (exact or len(dp.layout.mirror_jac))
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    n = (model.ncon, model.plan.n_jac_slots, model.plan.n_hess_slots)
+    d = [torch.empty(k, dtype=torch.float64, device=dev) for k in n]
+    xd, yd = torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev)
+    st = torch.cuda.Stream(dev)
+    sh = C.c_void_p(st.cuda_stream)
+    _lib.check(lib.exa_eval_set(dp.handle, None, xd.data_ptr(), yd.data_ptr(), w, *(t.data_ptr() for t in d), sh),
+               "set")
+    st.synchronize()
+    ref = [t.cpu().numpy().view(np.int64) for t in d]
+    wsp = C.c_void_p()
+    _lib.check(lib.exa_workspace_create(dp.handle, C.byref(wsp)), "workspace")
+    hx, hy = torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory()
+    h = [torch.full((k,), float("nan"), dtype=torch.float64).pin_memory() for k in n]
+    for flags in (0, _lib.WS_SYNC_HOST, 0):  # mirrors as a stream host step / written by the call
+        _lib.check(lib.exa_workspace_set_flags(wsp, flags), "flags")
+        for t in h:
+            t.fill_(float("nan"))
+        _lib.check(lib.exa_eval_set_host(dp.handle, wsp, hx.data_ptr(), hy.data_ptr(), w,
+                                         *(t.data_ptr() for t in h), sh), "set_host")
+        st.synchronize()
+        for a, r in zip(h, ref):
+            assert np.array_equal(a.numpy().view(np.int64), r)
+    hj = torch.full((n[1],), float("nan"), dtype=torch.float64).pin_memory()
+    hh = torch.full((n[2],), float("nan"), dtype=torch.float64).pin_memory()
+    _lib.check(lib.exa_eval_jac_host(dp.handle, wsp, hx.data_ptr(), hj.data_ptr(), sh), "jac_host")
+    _lib.check(lib.exa_eval_hess_host(dp.handle, wsp, hx.data_ptr(), hy.data_ptr(), w, hh.data_ptr(), sh), "hess_host")
+    st.synchronize()
+    assert np.array_equal(hj.numpy().view(np.int64), ref[1])
+    assert np.array_equal(hh.numpy().view(np.int64), ref[2])
+    # pageable numpy outputs (pinned staging, chunked copies, then the mirrors)
+    p = [np.full(k, np.nan) for k in n]
+    _lib.check(lib.exa_eval_set_host(dp.handle, wsp, x.ctypes.data, y.ctypes.data, w, *(a.ctypes.data for a in p),
+                                     sh), "set_host pageable")
+    st.synchronize()
+    for a, r in zip(p, ref):
+        assert np.array_equal(a.view(np.int64), r)
+    lib.exa_workspace_destroy(wsp)

@@ -56,6 +56,18 @@ def comp(i, jpat=True, hpat=True):
         lib.exa_last_error()
 
 
+WS = C.c_void_p()
+assert lib.exa_workspace_create(plans[0].handle, C.byref(WS)) == 0
+
+
+def comp_ws(i):
+    """one workspace (one raw-slot scratch) for every replica, as a solver
+    evaluating one model uses: inputs, parameters and outputs still rotate"""
+    b, p = bufs[i % R], plans[i % R]
+    assert lib.exa_eval_set_compressed(p.handle, WS, hj[i % R], hh[i % R], b["x"].data_ptr(), b["y"].data_ptr(),
+                                       b["w"], b["c"].data_ptr(), b["Jc"].data_ptr(), b["Hc"].data_ptr(), sh) == 0
+
+
 def graph_us(fn, n=8 * R, reps=5):
     with torch.cuda.stream(st):
         for i in range(R):
@@ -85,6 +97,7 @@ if os.environ.get("EXA_NCU") == "1":
     torch.cuda.synchronize()
     sys.exit(0)
 out = {"workload": name, "R": R, "set_us": graph_us(set_only), "set_comp_us": graph_us(comp),
+       "set_comp_shared_ws_us": graph_us(comp_ws),
        "set_compJ_us": graph_us(lambda i: comp(i, True, False)),
        "set_compH_us": graph_us(lambda i: comp(i, False, True)),
        "nnz_jac": jp.nnz, "nnz_hess": hp.nnz, "env": {k: v for k, v in os.environ.items() if k.startswith("EXA_")}}
