@@ -493,8 +493,8 @@ def compressed_leg(model, plans, bufs, lib, stream, dev, peak):
                              bufs[0]["Hc"].cpu().numpy().view(np.uint64)))
     a = algorithmic_bytes(model)
     cb = a["total"] - a["jac"] - a["hess"] + 8 * (jp.nnz + hp.nnz)
-    # host buffers, 3 streams in round robin (pinned), copies inside the timed region
-    NS = 3
+    # host buffers, 4 streams in round robin (pinned), copies inside the timed region
+    NS = 4
     slots = []
     for k in range(NS):
         wsp = C.c_void_p()
@@ -517,7 +517,7 @@ def compressed_leg(model, plans, bufs, lib, stream, dev, peak):
         issue(i)
     for sl in slots:
         sl["st"].synchronize()
-    n = 48
+    n = 192
     t0 = time.perf_counter()
     for i in range(n):
         issue(i)
@@ -531,7 +531,7 @@ def compressed_leg(model, plans, bufs, lib, stream, dev, peak):
             "bit_equal_sum_values": ok,
             "e2e": {"value": e2e, "unit": "sets/s", "h2d_bytes_per_step": 8 * (model.nvar + model.ncon),
                     "d2h_bytes_per_step": 8 * (model.ncon + jp.nnz + hp.nnz),
-                    "path": "exa_eval_set_compressed_host, pinned buffers, 3 streams in round robin"},
+                    "path": "exa_eval_set_compressed_host, pinned buffers, 4 streams in round robin"},
             "note": "bytes = x + y + parameters + c + compressed J and H (SURVEY 8d compressed variant); "
                     "raw J/H live in workspace scratch (read back from L2 by the segmented sum)"}
 
@@ -727,7 +727,7 @@ def main():
     # NS slots (workspace + stream + pinned host buffers) in round robin, so set
     # i+1's copies overlap set i's (PCIe is full duplex).  Every step copies its
     # inputs in and its full result out inside the timed region.
-    NS = 3
+    NS = 4
     xh, yh = eval_inputs(model, 7)[:2]
     slots = []
     for k in range(NS):
@@ -758,7 +758,7 @@ def main():
     e2e_sync()
     # the pipelined host path returns the same bits as the device path
     assert np.array_equal(slots[0]["c"].numpy(), slots[1]["c"].numpy())
-    n_e2e = max(1, args.e2e_steps) * 8 * NS
+    n_e2e = max(1, args.e2e_steps) * 32 * NS
     if ws > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
@@ -792,9 +792,7 @@ def main():
     assert np.array_equal(Hp_, Hn) and np.array_equal(Jp_, Jn)
     # the host path's H equals the device path's bit for bit (host-filled runs included)
     assert np.array_equal(slots[0]["H"].numpy().view(np.uint64), slots[1]["H"].numpy().view(np.uint64))
-    # latency view: one set at a time, synchronised per set (a synchronous
-    # caller's workspace: the call itself waits and writes the host mirrors)
-    _lib.check(lib.exa_workspace_set_flags(slots[0]["ws"], _lib.WS_SYNC_HOST), "workspace flags")
+    # latency view: one set at a time, synchronised per set
     t0 = time.perf_counter()
     for i in range(n_e2e // NS):
         e2e_issue(0)
@@ -814,10 +812,7 @@ def main():
     lay0 = plans[0].layout
     filled = 8 * int(lay0.fill_jac[:, 1].sum() + (lay0.fill_hess[:, 1].sum() if len(lay0.fill_hess) else 0)
                      + (lay0.fill_wzero[:, 1].sum() if len(lay0.fill_wzero) else 0))
-    # ... and the mirror runs (exact +-copies of a copied run) are written by
-    # host threads from the arrived source, also inside the call
-    mirrored = 8 * int(sum(int(m[:, 1].sum()) for m in (lay0.mirror_jac, lay0.mirror_hess) if len(m)))
-    d2h = 8 * (model.ncon + model.plan.n_jac_slots + model.plan.n_hess_slots) - filled - mirrored
+    d2h = 8 * (model.ncon + model.plan.n_jac_slots + model.plan.n_hess_slots) - filled
 
     if rank != 0:
         if ws > 1:
@@ -853,10 +848,9 @@ def main():
         "e2e": {"value": e2e_value, "unit": "sets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": (f"exa_eval_set_host (C ABI): pinned host x,y -> HBM -> set kernel -> pinned host c,J,H; "
                          f"one set per step, {NS} streams in round robin; constant / weighted-zero J/H runs "
-                         f"({filled / 1e6:.1f} MB) and exact +-copies of copied runs ({mirrored / 1e6:.1f} MB) "
-                         f"written by host threads, not copied; D2H by one store kernel into the mapped arrays"),
+                         f"({filled / 1e6:.1f} MB) written by host threads, not copied; D2H by one store "
+                         f"kernel into the mapped arrays"),
                 "host_filled_bytes_per_step": filled,
-                "host_mirrored_bytes_per_step": mirrored,
                 "d2h_GBps": d2h * e2e_value / (1 if sharded else ws) / 1e9,
                 "sequential_value": e2e_seq, "numpy_api_value": e2e_numpy,
                 "numpy_api_pinned_value": e2e_numpy_pinned},

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define EXA_ABI_VERSION 7
+#define EXA_ABI_VERSION 6
 #define EXA_MAXF 16
 #define EXA_MAXI 16
 #define EXA_MAXK 16
@@ -142,16 +142,6 @@ typedef struct ExaPlanDesc {
   int32_t n_wzero, pad_wz;
   const int32_t* host_wzero_rows;
   int64_t n_wzero_rows;
-  /* host path: raw J / H slot runs that are exact copies or negations of
-     another run of the same output on every call (one record's outputs with
-     equal sign-factored expressions, e.g. dp/dva_t = -dp/dva_f of a polar
-     flow), int64 quadruples (first slot, length, first source slot, sign
-     +-1): the first n_mirror_jac index J, the next n_mirror_hess index H,
-     sorted, disjoint from every fill run and from each other; sources lie in
-     copied ranges.  Written on the host as dst = sign * src (NaN copied
-     as is) once the source has arrived, instead of crossing PCIe.  May be 0. */
-  const int64_t* host_mirror;
-  int32_t n_mirror_jac, n_mirror_hess;
 } ExaPlanDesc;
 
 /* ---- build-time: JIT ---------------------------------------------------- */
@@ -166,13 +156,6 @@ void exa_plan_destroy(ExaPlan* plan);
 int exa_plan_info(const ExaPlan* plan, int64_t* bytes_device, int32_t* regs_set_kernel);
 int exa_workspace_create(ExaPlan* plan, ExaWorkspace** out);
 void exa_workspace_destroy(ExaWorkspace* ws);
-/* Workspace flags.  EXA_WS_SYNC_HOST: host-buffer calls on this workspace
- * return with their outputs complete (the call waits for its stream, then
- * writes the host mirror runs itself) -- for synchronous callers such as the
- * numpy API; without it the mirrors are a host function on the stream
- * (asynchronous, best when several workspaces / streams are in flight). */
-#define EXA_WS_SYNC_HOST 1
-int exa_workspace_set_flags(ExaWorkspace* ws, int32_t flags);
 
 /* ---- the callbacks (device pointers) ------------------------------------ */
 int exa_eval_obj(ExaPlan* plan, ExaWorkspace* ws, const double* x, double* out_scalar,

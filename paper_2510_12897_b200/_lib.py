@@ -16,8 +16,7 @@ MAXF = MAXI = MAXK = 16
 NMODES = 6
 NKERN = 12
 MODE_SET, MODE_CONS, MODE_JAC, MODE_HESS, MODE_OBJV, MODE_GRAD = range(6)
-ABI_VERSION = 7
-WS_SYNC_HOST = 1  # exa_workspace_set_flags: host-buffer calls return complete
+ABI_VERSION = 6
 
 i64, i32, dbl, vp = C.c_int64, C.c_int32, C.c_double, C.c_void_p
 
@@ -53,7 +52,6 @@ class PlanDesc(C.Structure):
         ("persist", i32 * NKERN), ("pdl", i32), ("batchable", i32), ("host_fill", C.POINTER(C.c_int64)), ("n_fill_jac", i32), ("n_fill_hess", i32),
         ("host_wzero", C.POINTER(C.c_int64)), ("n_wzero", i32), ("pad_wz", i32),
         ("host_wzero_rows", C.POINTER(C.c_int32)), ("n_wzero_rows", i64),
-        ("host_mirror", C.POINTER(C.c_int64)), ("n_mirror_jac", i32), ("n_mirror_hess", i32),
     ]
 
 
@@ -68,7 +66,6 @@ SIGNATURES = {
     "exa_plan_info": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i32)]),
     "exa_workspace_create": (C.c_int, [vp, C.POINTER(vp)]),
     "exa_workspace_destroy": (None, [vp]),
-    "exa_workspace_set_flags": (C.c_int, [vp, i32]),
     "exa_eval_obj": (C.c_int, [vp, vp, vp, vp, vp]),
     "exa_eval_grad": (C.c_int, [vp, vp, vp, vp, vp]),
     "exa_eval_cons": (C.c_int, [vp, vp, vp, vp, vp]),

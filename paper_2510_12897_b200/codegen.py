@@ -59,9 +59,6 @@ _DERIV_ZERO_ELISION = os.environ.get("EXA_EXACT_ZERO_SIGN", "0") != "1"
 # -> 38.9); balance-row multipliers (augments, row buckets) are shared and
 # keep __ldg
 _WGT_CS = os.environ.get("EXA_WGT_CS", "1") == "1"
-# term groups that evaluate sin/cos prefetch the sin/cos table into L1 before
-# their grid-dependency wait (EXA_SC_PREFETCH in exa_math.h)
-_SC_PF = os.environ.get("EXA_SC_PF", "0") == "1"
 
 
 class Arr:
@@ -136,11 +133,8 @@ class Gen:
         # derivative-space emission (see bin add); off while emitting values
         self.deriv = False
         self.checks: list = []
-        # name -> ("neg", a) | ("mul" | "div", a, b): the operations whose sign
-        # factors out exactly (see sig)
-        self.struct: dict = {}
 
-    def new(self, expr: str, nz: bool = False, struct=None) -> Sym:
+    def new(self, expr: str, nz: bool = False) -> Sym:
         got = self.memo.get(expr)
         if got is not None:
             return got
@@ -149,31 +143,7 @@ class Gen:
         self.lines.append(f"  const double {name} = {expr};")
         s = Sym(name, nz)
         self.memo[expr] = s
-        if struct is not None:
-            self.struct[name] = struct
         return s
-
-    def sig(self, v):
-        """(sign, key) with value(v) == sign * value(key) bit for bit for every
-        input: negation flips the sign bit, and the sign of a product or a
-        quotient is the xor of its operands' signs (IEEE-754, zeros and
-        infinities included; NaNs stay NaNs).  Sums are opaque: -(a + b) and
-        (-a) + (-b) differ in the sign of an exactly cancelling zero.  Two
-        outputs with equal keys are exact (+-) copies of each other."""
-        if not isinstance(v, Sym):
-            c = float(v.value if isinstance(v, Arr) else v)
-            return (-1 if math.copysign(1.0, c) < 0 else 1), ("c", abs(c).hex())
-        st = self.struct.get(v.name)
-        if st is None:
-            return 1, v.name
-        if st[0] == "neg":
-            s_, k_ = self.sig(st[1])
-            return -s_, k_
-        sa, ka = self.sig(st[1])
-        sb, kb = self.sig(st[2])
-        if st[0] == "mul" and repr(kb) < repr(ka):  # a * b == b * a exactly
-            ka, kb = kb, ka
-        return sa * sb, (st[0], ka, kb)
 
     @staticmethod
     def r(v) -> str:
@@ -219,7 +189,7 @@ class Gen:
                 return b
         sym = {"add": "+", "sub": "-", "mul": "*", "div": "/"}[op]
         nz = (op == "add" and (_nz(a) or _nz(b))) or (op == "sub" and _nz(a))
-        out = self.new(f"{self.r(a)} {sym} {self.r(b)}", nz, (op, a, b) if op in ("mul", "div") else None)
+        out = self.new(f"{self.r(a)} {sym} {self.r(b)}", nz)
         if op == "sub":
             self.diffs[out.name] = (self.r(a), self.r(b))
         return out
@@ -238,7 +208,7 @@ class Gen:
 
     def neg(self, a):
         if isinstance(a, Sym):
-            return self.new(f"-{a.name}", struct=("neg", a))
+            return self.new(f"-{a.name}")
         if isinstance(a, Arr):
             return Arr(-a.value)
         return float(-np.float64(a))
@@ -259,7 +229,7 @@ class Gen:
                 other = self.memo.get(f"{rhs} - {lhs}")
                 if other is not None and other.name in self.sincos:
                     s_o, c_o = self.sincos[other.name]
-                    pair = (self.new(f"-{s_o.name}", struct=("neg", s_o)), c_o)
+                    pair = (self.new(f"-{s_o.name}"), c_o)
                     self.sincos[a.name] = pair
             if pair is None:
                 s, c = f"s_{a.name}", f"c_{a.name}"
@@ -624,32 +594,6 @@ class PatternCode:
                     (self.hzero if self.relax else self.hzero_w).append(
                         pair if self.relax else (pair, float(val.value if isinstance(val, Arr) else val)))
                 pair += 1
-        # exact (+-) copies among the x-dependent outputs of one record (equal
-        # sign-factored keys, Gen.sig): J slot s == sign * J slot src, H pair p
-        # == sign * H pair src (same weight; pairs that double on a duplicate
-        # variable are left out).  The host path copies only the first of each
-        # class over PCIe and writes the others on the host (host mirrors).
-        self.jmirror, self.hmirror = {}, {}
-        seen: dict = {}
-        for s in range(k):
-            if isinstance(grads[s], Sym):
-                sg, key = g.sig(grads[s])
-                if key in seen:
-                    self.jmirror[s] = (seen[key][0], sg * seen[key][1])
-                else:
-                    seen[key] = (s, sg)
-        seen, pair = {}, 0
-        for i in range(k):
-            for j in range(i + 1):
-                val = by_seed[j][i]
-                dup = i != j and self.slot_struct[i][0] == self.slot_struct[j][0]
-                if not dup and not _zero_const(val):  # wgt * c: constants mirror too
-                    sg, key = g.sig(val)
-                    if key in seen:
-                        self.hmirror[pair] = (seen[key][0], sg * seen[key][1])
-                    else:
-                        seen[key] = (pair, sg)
-                pair += 1
 
         out = []
         pid = self.pid
@@ -883,8 +827,6 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
            "  double* __restrict__ Hout = A.H;", "  int rank = rank0;"]
     out.extend(pre)
     out.append(f"  EXA_TP(0, i{min(u_src)});" if u_src else "  EXA_TP(0, 0.0);")
-    if _SC_PF and g.sincos:
-        out.append("  EXA_SC_PREFETCH();")
     out.append("  EXA_GRID_WAIT();")
     out.extend(post)
     out.extend(early)

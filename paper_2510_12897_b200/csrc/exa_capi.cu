@@ -19,8 +19,6 @@
 #include <cstdlib>
 #include <algorithm>
 #include <atomic>
-#include <memory>
-#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstring>
@@ -97,7 +95,6 @@ struct ExaWorkspace {
   /* guards the lazy staging allocation (a workspace serves one evaluation at
      a time; concurrent callers use one workspace each) */
   std::mutex mu;
-  int32_t flags = 0; /* EXA_WS_* */
 };
 
 struct ExaObjNode;
@@ -140,7 +137,6 @@ struct ExaPlan {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern[EXA_NKERN] = {};
   cudaKernel_t kern_batch = nullptr; /* strided-batch set kernel (parameters kept in L2), if the module has one */
-  cudaKernel_t kern_keep[2] = {};    /* set kernels that keep raw J / H in L2 (compressed sets), if present */
   ExaWorkspace* dflt = nullptr;
   size_t bytes = 0;
   int pdl = 0;
@@ -152,10 +148,6 @@ struct ExaPlan {
   struct WRun { int64_t a, n, off; double z; };
   std::vector<WRun> fill_wz;
   std::vector<int32_t> wz_rows;
-  /* ... and mirror runs: slot a + i = sign * slot src + i (host-written once
-     the source has arrived) */
-  struct MRun { int64_t a, n, src; int sign; };
-  std::vector<MRun> mir_jac, mir_hess;
   /* ... and the complementary slot ranges copied D2H, (first, length) */
   std::vector<std::pair<int64_t, int64_t>> copy_jac, copy_hess;
   /* the same ranges (c whole, then J, then H) cut into CTA chunks for the
@@ -823,13 +815,6 @@ void exa_workspace_destroy(ExaWorkspace* w) {
   delete w;
 }
 
-int exa_workspace_set_flags(ExaWorkspace* ws, int32_t flags) {
-  if (!ws) return fail("exa_workspace_set_flags: null workspace");
-  if (flags & ~EXA_WS_SYNC_HOST) return fail("exa_workspace_set_flags: unknown flags 0x%x", flags);
-  ws->flags = flags;
-  return 0;
-}
-
 int exa_workspace_create(ExaPlan* p, ExaWorkspace** out) {
   if (!p || !out) return fail("exa_workspace_create: null argument");
   CU(cudaSetDevice(p->device));
@@ -929,15 +914,6 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
       for (int32_t r : p->wz_rows)
         if (r < 0 || r >= d->ncon) return bail(fail("host_wzero_rows: row out of range"));
     }
-    const int nmj = d->host_mirror ? d->n_mirror_jac : 0, nmh = d->host_mirror ? d->n_mirror_hess : 0;
-    for (int i = 0; i < nmj + nmh; ++i) {
-      const int64_t* q = d->host_mirror + 4 * i;
-      const int64_t total = i < nmj ? d->n_jac : d->n_hess;
-      if (q[1] <= 0 || q[0] < 0 || q[0] + q[1] > total || q[2] < 0 || q[2] + q[1] > total || (q[3] != 1 && q[3] != -1))
-        return bail(fail("host_mirror: run out of range"));
-      (i < nmj ? p->mir_jac : p->mir_hess).push_back({q[0], q[1], q[2], (int)q[3]});
-      (i < nmj ? sj : sh).push_back({q[0], q[1]});
-    }
     if ((rc = complement(sj, d->n_jac, p->copy_jac))) return bail(rc);
     if ((rc = complement(sh, d->n_hess, p->copy_hess))) return bail(rc);
     // constant runs shorter than EXA_D2H_GAP slots between two copied ranges
@@ -967,18 +943,6 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
       drop(p->fill_jac, p->copy_jac);
       drop(p->fill_hess, p->copy_hess);
       drop(p->fill_wz, p->copy_hess);
-      drop(p->mir_jac, p->copy_jac);
-      drop(p->mir_hess, p->copy_hess);
-    }
-    // a mirror's source must cross PCIe (lie inside one copied range)
-    for (int k = 0; k < 2; ++k) {
-      const auto& cp = k ? p->copy_hess : p->copy_jac;
-      for (const auto& m : k ? p->mir_hess : p->mir_jac) {
-        auto it = std::upper_bound(cp.begin(), cp.end(), std::make_pair(m.src, INT64_MAX));
-        if (it == cp.begin() || m.src + m.n > std::prev(it)->first + std::prev(it)->second)
-          return bail(fail("host_mirror: source run [%lld, %lld) is not copied", (long long)m.src,
-                           (long long)(m.src + m.n)));
-      }
     }
     {
       auto ops = [&](int arr, const std::vector<std::pair<int64_t, int64_t>>& cp) {
@@ -1130,11 +1094,6 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
     cudaGetLastError();
     p->kern_batch = nullptr;
   }
-  for (int h = 0; h < 2; ++h)
-    if (cudaLibraryGetKernel(&p->kern_keep[h], p->lib, h ? "exa_k_setk_l" : "exa_k_setk_h") != cudaSuccess) {
-      cudaGetLastError();
-      p->kern_keep[h] = nullptr;
-    }
   if ((rc = ws_alloc(p, &p->dflt))) return bail(rc);
   *out = p;
   return 0;
@@ -1152,8 +1111,7 @@ int exa_plan_info(const ExaPlan* p, int64_t* bytes, int32_t* regs) {
   return 0;
 }
 
-static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStream_t st, unsigned nbatch = 1,
-                      bool keep = false) {
+static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStream_t st, unsigned nbatch = 1) {
   const ExaTerm* terms = p->terms;
   const ExaSeg* segs = p->segs[kid];
   const int* cmap = p->cta_seg[kid];
@@ -1172,16 +1130,13 @@ static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStrea
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool batch_kernel = nbatch > 1 && kid == 2 * EXA_MODE_SET + 1 && p->kern_batch;
-  cudaKernel_t k = batch_kernel ? p->kern_batch : p->kern[kid];
-  if (keep && nbatch == 1 && kid / 2 == EXA_MODE_SET && p->kern_keep[kid & 1]) k = p->kern_keep[kid & 1];
-  CU(cudaLaunchKernelExC(&cfg, (const void*)k, args));
+  CU(cudaLaunchKernelExC(&cfg, (const void*)(batch_kernel ? p->kern_batch : p->kern[kid]), args));
   return 0;
 }
 
 // One callback = its heavy kernel on `st` and its light kernel on the
 // workspace's aux stream, forked/joined with events (graph-capturable).
-static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaStream_t st, unsigned nbatch = 1,
-                       bool keep = false) {
+static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaStream_t st, unsigned nbatch = 1) {
   A.err = w->err;
   A.trace = g_trace;
   A.obj_base = p->err_base[mode][0];
@@ -1196,14 +1151,14 @@ static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaSt
     // light kernel's many short CTAs fill every SM
     CU(cudaEventRecord(w->fork, st));
     CU(cudaStreamWaitEvent(w->aux, w->fork, 0));
-    if ((rc = launch_kid(p, w, kh, A, st, nbatch, keep))) return rc;
-    if ((rc = launch_kid(p, w, kl, A, w->aux, nbatch, keep))) return rc;
+    if ((rc = launch_kid(p, w, kh, A, st, nbatch))) return rc;
+    if ((rc = launch_kid(p, w, kl, A, w->aux, nbatch))) return rc;
     CU(cudaEventRecord(w->join, w->aux));
     CU(cudaStreamWaitEvent(st, w->join, 0));
   } else if (h) {
-    rc = launch_kid(p, w, kh, A, st, nbatch, keep);
+    rc = launch_kid(p, w, kh, A, st, nbatch);
   } else if (l) {
-    rc = launch_kid(p, w, kl, A, st, nbatch, keep);
+    rc = launch_kid(p, w, kl, A, st, nbatch);
   }
   return rc;
 }
@@ -1236,8 +1191,8 @@ struct DeviceGuard {
   memset(&A, 0, sizeof A);                                  \
   if (int rc_ = reset_err(p, w, st)) return rc_;
 
-static int eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
-                    double* jac, double* hess, exa_stream_t stream, bool keep) {
+int exa_eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
+                 double* jac, double* hess, exa_stream_t stream) {
   EXA_PROLOGUE();
   A.x = x;
   A.y = mult;
@@ -1245,12 +1200,7 @@ static int eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double*
   A.c = c;
   A.J = jac;
   A.H = hess;
-  return launch_mode(p, w, EXA_MODE_SET, A, st, 1, keep);
-}
-
-int exa_eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
-                 double* jac, double* hess, exa_stream_t stream) {
-  return eval_set(p, ws, x, mult, w_obj, c, jac, hess, stream, false);
+  return launch_mode(p, w, EXA_MODE_SET, A, st);
 }
 
 int exa_eval_set_batch(ExaPlan* p, ExaWorkspace* ws, int64_t nsets, const double* x, const double* mult,
@@ -1279,7 +1229,6 @@ struct FillPool {
   struct Piece {
     double* dst; int64_t n; double v; const double* src = nullptr; cudaEvent_t ev = nullptr;
     const int32_t* rows = nullptr; const double* mult = nullptr;  // weighted zeros: dst[i] = mult[rows[i]] * v
-    bool neg = false;  // (src) mirror: dst[i] = -src[i], NaN copied as is
   };
   std::mutex call_mu;  // one fill at a time
   std::mutex mu;
@@ -1287,19 +1236,12 @@ struct FillPool {
   std::vector<std::thread> workers;
   const std::vector<Piece>* job = nullptr;
   uint64_t gen = 0;
-  std::atomic<uint64_t> agen{0};  // gen, readable without the lock (spinning workers)
-  int spin_us = 200;              // EXA_HOST_SPIN_US: workers spin this long before sleeping
   std::atomic<size_t> next{0};
   std::atomic<int> active{0};
 
   static void run(const Piece& q) {
     if (q.rows) {
       for (int64_t i = 0; i < q.n; ++i) q.dst[i] = q.mult[q.rows[i]] * q.v;
-    } else if (q.src && q.neg) {
-      for (int64_t i = 0; i < q.n; ++i) {
-        const double v = q.src[i];
-        q.dst[i] = v != v ? v : -v;
-      }
     } else if (q.src) {
       if (q.ev) cudaEventSynchronize(q.ev);
       std::memcpy(q.dst, q.src, q.n * sizeof(double));
@@ -1313,18 +1255,11 @@ struct FillPool {
     for (size_t i; (i = next.fetch_add(1)) < pcs.size();) run(pcs[i]);
   }
   explicit FillPool(int n) {
-    if (const char* e = std::getenv("EXA_HOST_SPIN_US")) spin_us = std::atoi(e);
     for (int t = 0; t < n; ++t)
       workers.emplace_back([this] {
         uint64_t seen = 0;
         for (;;) {
           const std::vector<Piece>* j;
-          // back-to-back calls (a solver's, every few hundred us) find the
-          // workers awake: a sleeping worker's wake-up costs tens of us on a VM
-          const auto t0 = std::chrono::steady_clock::now();
-          while (agen.load(std::memory_order_acquire) == seen &&
-                 std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(spin_us))
-            __builtin_ia32_pause();
           {
             std::unique_lock<std::mutex> lk(mu);
             cv.wait(lk, [&] { return gen != seen; });
@@ -1348,7 +1283,6 @@ struct FillPool {
         std::lock_guard<std::mutex> lk(mu);
         job = &pcs;
         ++gen;
-        agen.store(gen, std::memory_order_release);
       }
       cv.notify_all();
       drain(pcs);
@@ -1398,36 +1332,6 @@ static void add_fill(const ExaPlan* p, double* jac, double* hess, const double* 
         pcs.push_back(q);
       }
     }
-}
-
-// mirror pieces of one host-path call: dst = sign * src within the caller's
-// J / H arrays (the sources are already there when they run)
-static void add_mirrors(const ExaPlan* p, double* jac, double* hess, std::vector<FillPool::Piece>& pcs) {
-  for (int k = 0; k < 2; ++k) {
-    double* out = k ? hess : jac;
-    if (!out) continue;
-    for (const auto& m : k ? p->mir_hess : p->mir_jac)
-      for (int64_t o = 0; o < m.n; o += kPiece) {
-        FillPool::Piece q{out + m.a + o, m.n - o < kPiece ? m.n - o : kPiece, 0.0, out + m.src + o};
-        q.neg = m.sign < 0;
-        pcs.push_back(q);
-      }
-  }
-}
-
-// EXA_MIRROR_SYNC=1: the call waits for its D2H and writes the mirrors itself
-// (no host function on the stream)
-static bool mirror_sync() {
-  static const bool v = [] { const char* e = std::getenv("EXA_MIRROR_SYNC"); return e && e[0] == '1'; }();
-  return v;
-}
-
-// stream-ordered host step: the mirror pieces run once the D2H before them
-// on the stream has landed (a host function; its pieces are freed here)
-static void CUDART_CB run_mirrors(void* job) {
-  auto* pcs = static_cast<std::vector<FillPool::Piece>*>(job);
-  fill_pool().fill(*pcs);
-  delete pcs;
 }
 
 static bool pageable(const void* ptr) {
@@ -1608,17 +1512,6 @@ static int host_eval(ExaPlan* p, ExaWorkspace* ws, int mode, const double* x, co
   }
   add_fill(p, jac, hess, mult, w_obj, pcs);
   if (!pcs.empty()) fill_pool().fill(pcs);
-  std::unique_ptr<std::vector<FillPool::Piece>> mir(new std::vector<FillPool::Piece>());
-  add_mirrors(p, jac, hess, *mir);
-  if (mir->empty()) return 0;
-  if (pg_out || (w->flags & EXA_WS_SYNC_HOST) || mirror_sync()) {  // pageable: the sources are there now
-    if (!pg_out) CU(cudaStreamSynchronize(st));
-    fill_pool().fill(*mir);
-    return 0;
-  }
-  if (cudaLaunchHostFunc(st, run_mirrors, mir.get()) != cudaSuccess)
-    return fail("cudaLaunchHostFunc: %s", cudaGetErrorString(cudaGetLastError()));
-  mir.release();  // run_mirrors frees it
   return 0;
 }
 
@@ -1800,10 +1693,7 @@ static int set_compressed(ExaPlan* p, ExaWorkspace* w, const ExaPattern* jp, con
   if (jp && hp && jp->ipt != hp->ipt) return fail("exa_eval_set_compressed: patterns chunked for different EXA_CMP_IPT");
   double* rawJ = jp ? w->dJ : jc;
   double* rawH = hp ? w->dH : hc;
-  // raw slots into the workspace's scratch, kept in L2 (plain stores): the
-  // segmented sum reads them back and the next set on this workspace
-  // overwrites them, so with EXA_SETK (default) they need never reach DRAM
-  int rc = eval_set(p, w, x, mult, w_obj, c, rawJ, rawH, st, jp && hp);
+  int rc = exa_eval_set(p, w, x, mult, w_obj, c, rawJ, rawH, st);
   if (rc) return rc;
   const int nchJ = jp ? jp->nch : 0, nchH = hp ? hp->nch : 0;
   if (nchJ + nchH == 0) return 0;

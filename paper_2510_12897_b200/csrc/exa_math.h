@@ -52,20 +52,6 @@
   const double C0h = EXA_SC(j, 2), C0l = EXA_SC(j, 3)
 #endif
 
-/* L1 prefetch of the whole table (15 lines of 128 B, one lane each), issued
-   by term groups after their parameter loads and before griddepcontrol.wait:
-   the table's first use per SM would otherwise be an L2 round trip on the
-   critical path behind the x gathers (EXA_SC_PF=1) */
-#if defined(__CUDACC_RTC__) || defined(__CUDACC__)
-#define EXA_SC_PREFETCH()                                                                                       \
-  do {                                                                                                         \
-    const unsigned l_ = threadIdx.x & 31u;                                                                     \
-    if (l_ < (unsigned)((EXA_SC_N * 32 + 127) / 128))                                                          \
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(__cvta_generic_to_global(                                 \
-                       reinterpret_cast<const char*>(&exa_sc_tab[0][0]) + 128 * l_)));                          \
-  } while (0)
-#endif
-
 typedef struct {
   double hi, lo;
 } exa_dd;

@@ -765,39 +765,7 @@ class HostLayout:
 
         self.fill_wzero = np.array(sorted(runs_w), dtype=np.int64).reshape(-1, 4)
         self.wz_rows = (np.concatenate(rows_pool) if rows_pool else np.zeros(0, dtype=np.int32)).astype(np.int32)
-        self.mirror_jac, self.mirror_hess = self._host_mirrors(terms)
         return merge(runs_j), merge(runs_h)
-
-    def _host_mirrors(self, terms):
-        """Runs of raw J / H slots that are exact (+-) copies of another run on
-        every call (``PatternCode.jmirror`` / ``hmirror``: equal sign-factored
-        expressions within one record), int64 quadruples (first slot, length,
-        first source slot, sign); the host path writes them as dst = sign * src
-        once the source has crossed PCIe.  ``EXA_HOST_MIRROR=0`` disables them."""
-        if os.environ.get("EXA_HOST_MIRROR", "1") != "1":
-            return np.zeros((0, 4), dtype=np.int64), np.zeros((0, 4), dtype=np.int64)
-        mj, mh = [], []
-        for t, tp in enumerate(terms):
-            pc = self.patterns[self.term_pid[t]]
-            d, n = self.descs[t], tp.nrec
-            if n == 0 or not pc.k:
-                continue
-            if tp.kind != "objective":
-                for s_, (src, sg) in pc.jmirror.items():
-                    mj.append((d["jac0"] + s_ * n, n, d["jac0"] + src * n, sg))
-            for pr, (src, sg) in pc.hmirror.items():
-                mh.append((d["hess0"] + pr * n, n, d["hess0"] + src * n, sg))
-
-        def merge(runs):  # adjacent runs whose sources are adjacent too, same sign
-            out = []
-            for a, n, src, sg in sorted(runs):
-                if out and out[-1][0] + out[-1][1] == a and out[-1][2] + out[-1][1] == src and out[-1][3] == sg:
-                    out[-1][1] += n
-                else:
-                    out.append([a, n, src, sg])
-            return np.array(out, dtype=np.int64).reshape(-1, 4)
-
-        return merge(mj), merge(mh)
 
     def _grad_csr(self, nvar):
         plan = self.plan
@@ -921,9 +889,6 @@ class DevicePlan:
         desc.n_wzero = len(lay.fill_wzero)
         desc.host_wzero_rows = self._wz_rows.ctypes.data_as(C.POINTER(C.c_int32))
         desc.n_wzero_rows = self._wz_rows.size
-        self._mir = np.ascontiguousarray(np.concatenate([lay.mirror_jac, lay.mirror_hess]).reshape(-1), dtype=np.int64)
-        desc.host_mirror = self._mir.ctypes.data_as(C.POINTER(C.c_int64))
-        desc.n_mirror_jac, desc.n_mirror_hess = len(lay.mirror_jac), len(lay.mirror_hess)
         n_obj, n_con = len(plan.obj_terms), len(plan.con_terms)
         bases = {
             _lib.MODE_SET: (n_con, 0), _lib.MODE_CONS: (0, 0), _lib.MODE_JAC: (0, 0),
@@ -970,8 +935,6 @@ class DevicePlan:
             ws = C.c_void_p()
             with torch.cuda.device(self.device):
                 _lib.check(self._lib.exa_workspace_create(self.handle, C.byref(ws)), "exa_workspace_create")
-            # the Python host-buffer calls are synchronous (numpy in, numpy out)
-            _lib.check(self._lib.exa_workspace_set_flags(ws, _lib.WS_SYNC_HOST), "exa_workspace_set_flags")
             with self._ws_lock:
                 self._workspaces.append(ws)
             self._tls.ws = ws

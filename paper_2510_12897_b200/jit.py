@@ -83,13 +83,11 @@ def _bkt_release(threads: int) -> int:
 PDL_MID = int(os.environ.get("EXA_PDL_MID", "1"))
 ST_CS = os.environ.get("EXA_ST_CS", "1") == "1"  # evict-first stores of the c / J / H outputs
 LD_CS = os.environ.get("EXA_LD_CS", "1") == "1"  # evict-first loads of the per-record parameters
-KEEP_VARIANT = os.environ.get("EXA_SETK", "1") == "1"  # set-kernel entries that keep raw J / H in L2
 _LD_RES = (re.compile(r"__ldg\((T\d*\.(?:f|ix)\[[^\]]*\] \+ (?:r|o))\)"),
            re.compile(r"__ldg\((reinterpret_cast<const int2\*>\(A\.i32 \+ \d+LL\) \+ [^;]*?)\)(?=;)"),
            re.compile(r"__ldg\((A\.i32 \+ \d+LL \+ q)\)"),
            re.compile(r"__ldg\(((?:T\d*|U\d+)\.rows \+ [^)]*)\)"))
-_ST_RE = re.compile(r"\b(Cout|A\.c)\[([^\]\[]*)\] = ([^;]*);")
-_ST_JH_RE = re.compile(r"\b(Jout|Hout)\[([^\]\[]*)\] = ([^;]*);")  # release point inside term groups (see EXA_GRID_RELEASE_MID)
+_ST_RE = re.compile(r"\b(Jout|Hout|Cout|A\.c)\[([^\]\[]*)\] = ([^;]*);")  # release point inside term groups (see EXA_GRID_RELEASE_MID)
 
 _lock = threading.Lock()
 _mem_cache: dict = {}
@@ -189,13 +187,8 @@ _PREFETCH = r"""
 // launch evaluates one set; the strided-batch kernel (LDH = 0) reads the same
 // parameters for every set of the launch, so there they stay in L2.  LDH is a
 // template parameter of the generated functions; this is the default outside.
-// Bit 2 of LDH keeps the J / H outputs in L2 (plain stores instead of
-// evict-first): the compressed-set kernel (exa_k_setk_*) writes the raw slots
-// into workspace scratch that its segmented sum reads right back and the next
-// set overwrites, so they need never reach DRAM.
 constexpr int LDH = 1;
-#define EXA_LDP(p) ((LDH & 1) ? __ldcs(p) : __ldg(p))
-#define EXA_STO(p, v) do { if (LDH & 2) *(p) = (v); else __stcs((p), (v)); } while (0)
+#define EXA_LDP(p) (LDH ? __ldcs(p) : __ldg(p))
 // Bulk L2 prefetch of the gathered inputs: CTA b < n prefetches chunk b of x
 // (then of y).  The first random gathers of a set would otherwise miss L2
 // (the previous set used other buffers) and go to DRAM one 32-B sector at a
@@ -390,7 +383,7 @@ def _specialised_kernels(layout) -> str:
             oc.append(f"{lab} exa_termx_{layout.term_pid[u]}(xv, w, jv, hv); j0 = {descs[u]['jac0']}LL;"
                       f" h0 = {descs[u]['hess0']}LL; break;")
         ocases = "\n".join(oc)
-        out.append(f"""template <int WJ, int WH, int LDH = 1>
+        out.append(f"""template <int WJ, int WH>
 __device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, const double w, const int rec, const ExaArgs& A) {{
   double jv, hv;
   long long j0, h0;
@@ -427,7 +420,6 @@ def _cache_hints(src: str) -> str:
     x and y keep ``__ldg`` (gathered, reused across records)."""
     if ST_CS:
         src = _ST_RE.sub(r"__stcs(&\1[\2], \3);", src)
-        src = _ST_JH_RE.sub(r"EXA_STO(&\1[\2], \3);", src)
     if LD_CS:
         for pat in _LD_RES:
             src = pat.sub(r"EXA_LDP(\1)", src)
@@ -481,7 +473,7 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, m):
     if want_v:
         L.append(f"      v = exa_bkval_T{t}(e, xv);")
     if want_j or want_h:
-        L.append(f"      if (e >= 0 && rc >= 0) exa_bkout_T{t}<{int(want_j)}, {int(want_h)}, LDH>(e, xv, wrow, rc, A);")
+        L.append(f"      if (e >= 0 && rc >= 0) exa_bkout_T{t}<{int(want_j)}, {int(want_h)}>(e, xv, wrow, rc, A);")
     L.append("    }")
     if want_v:
         if LW == 32:
@@ -588,7 +580,7 @@ def _kernel_source(layout, m, half, kname) -> str:
                             b_.append(f"    acc = e{k} >= 0 ? acc + v{k} : acc;")
                     if want_j or want_h:
                         cond = f"if (rc{k} >= 0) " if k < always else f"if (e{k} >= 0 && rc{k} >= 0) "
-                        b_.append(f"    {cond}exa_bkout_T{t}<{int(want_j)}, {int(want_h)}, LDH>(e{k}, xv{k}, wrow, rc{k}, A);")
+                        b_.append(f"    {cond}exa_bkout_T{t}<{int(want_j)}, {int(want_h)}>(e{k}, xv{k}, wrow, rc{k}, A);")
             if want_v:
                 b_.append("    A.c[T.row_offset + r] = acc;")
             b_.append("    return;")
@@ -675,8 +667,6 @@ def _kernel_source(layout, m, half, kname) -> str:
     out = "\n".join(fn_body) + "\n" + entry.replace("@LDH@", "1")
     if m == 0 and half == 1:  # strided-batch entry (exa_eval_set_batch): parameters stay in L2
         out += "\n" + entry.replace("@LDH@", "0").replace(f" {kname}(", f" {kname.replace('_set_', '_setb_')}(", 1)
-    if m == 0 and KEEP_VARIANT:  # compressed-set entry (exa_eval_set_compressed): raw J / H stay in L2
-        out += "\n" + entry.replace("@LDH@", "3").replace(f" {kname}(", f" {kname.replace('_set_', '_setk_')}(", 1)
     return out
 
 

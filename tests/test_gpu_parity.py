@@ -248,10 +248,9 @@ def test_domain_error_in_constraint_block_order():
 def test_host_buffer_c_abi_matches_oracle(name):
     """exa_eval_set_host (pinned host in/out, copies on the stream) returns the
     CR oracle's bits, across two workspaces on the legacy default stream and a
-    side stream (D2H store kernel into the mapped arrays, host mirrors as a
-    stream-ordered host step).  The host buffers start as NaN: the constant
-    runs and mirrors written on the host plus the copied ranges cover every
-    slot."""
+    side stream (D2H store kernel into the mapped arrays).  The host buffers
+    start as NaN: the constant runs written on the host plus the copied
+    ranges cover every slot."""
     import ctypes as C
 
     import torch
