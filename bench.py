@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="headline and e2e only")
+    ap.add_argument("--shard-projection", action="store_true",
+                    help="also time every rank's shard of 2/4/8-way MP96 / N-1 splits alone on this GPU")
     ap.add_argument("--sharded-legs", action="store_true", help="(no-op: the other configs always run unless --no-extras)")
     return ap.parse_args()
 
@@ -373,13 +375,14 @@ def isolated_latency_us(launch, stream, dev, n=40):
     return statistics.median(out[5:])
 
 
-def sharded_leg(name, rank, ws, local, n_sets=8, steps=5, peak=None):
+def sharded_leg(name, rank, ws, local, n_sets=8, steps=5, peak=None, alone=False):
     """One BASELINE config measured in this run.  At N > 1 a batched config is
     sharded over the ranks (strong scaling): this rank's shard of ONE
     instance, timed sets (max over ranks), plus one ShardComm.exchange round
     (NCCL P2P halo) and one objective reduction (NCCL all-gather).  At N = 1
     it is the whole instance on this GPU (the config's own bench line, as an
-    extra key of the headline run)."""
+    extra key of the headline run).  ``alone``: rank ``rank``'s shard of a
+    ``ws``-way split timed on this one GPU (no collectives; shard projection)."""
     import numpy as np
     import torch
 
@@ -395,6 +398,8 @@ def sharded_leg(name, rank, ws, local, n_sets=8, steps=5, peak=None):
     comm = None
     if ws == 1 or "_" not in name:
         model = build_workload(name, lower_to_gpu=False)
+    elif alone:
+        model = build_workload(name, lower_to_gpu=False, rank=rank, world=ws)
     else:
         head, base = name.split("_", 1)
         if head.startswith("n1"):
@@ -416,7 +421,7 @@ def sharded_leg(name, rank, ws, local, n_sets=8, steps=5, peak=None):
     lib = _lib.load()
     stream = torch.cuda.Stream(dev)
     launch = launcher(lib, plans, bufs, stream)
-    if ws > 1:
+    if ws > 1 and not alone:
         torch.distributed.barrier()
     us = graph_us(launch, n_sets * R, stream, dev, reps=steps)
     out = {"workload": name, "shard_bytes_per_set": summ["bytes_per_set"], "replicas": R, "build_s": t_build}
@@ -721,6 +726,22 @@ def main():
         names = (("case1354", "mp96_case1354", "scen96_case1354", "n1_case2000") if ws == 1
                  else ("mp96_case1354", "scen96_case1354", "n1_case2000"))
         sharded_out = [sharded_leg(name, rank, ws, local, peak=peak) for name in names]
+        if ws == 1 and args.shard_projection:
+            # every rank's shard of a 2/4/8-way split, each timed alone on this
+            # GPU: the compute side of the strong-scaling runs (the sharded sets
+            # carry no collective; the halo / objective reductions are timed in
+            # the multi-GPU legs)
+            for leg in sharded_out:
+                if leg["workload"] in ("mp96_case1354", "n1_case2000"):
+                    proj = {}
+                    for n in (2, 4, 8):
+                        us = [sharded_leg(leg["workload"], r, n, local, alone=True)["max_rank_us_per_set"]
+                              for r in range(n)]
+                        proj[str(n)] = {"max_shard_us_per_set": max(us), "min_shard_us_per_set": min(us)}
+                    leg["shard_projection"] = {
+                        "by_n_shards": proj,
+                        "note": "each rank's shard of an N-way split timed alone on this one GPU "
+                                "(compute only; no per-set collective on the sharded path)"}
 
     # ---- end to end: host buffers through the C ABI, copies inside the timed region.
     # exa_eval_set_host = H2D(x, y) + set kernel + D2H(c, J, H) on one stream;
