@@ -194,7 +194,7 @@ def _host_outputs(*outs) -> bool:
     """Outputs the C ABI host path can write directly: contiguous, writable
     float64 numpy arrays."""
     return all(isinstance(b, np.ndarray) and b.dtype == np.float64 and b.flags.c_contiguous and b.flags.writeable
-               for b in outs)
+               and b.flags.aligned for b in outs)
 
 
 def _host_call(dp, name: str, callback: str, *args) -> None:

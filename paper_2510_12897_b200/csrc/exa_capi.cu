@@ -1370,9 +1370,10 @@ __global__ void __launch_bounds__(128) exa_d2h_store(const ExaD2HChunk* __restri
   }
 }
 
-// device address of a page-locked host array, or null (pageable / not mapped)
+// device address of a page-locked host array, or null (pageable / not mapped /
+// not 8-byte aligned: those take the copy-engine path)
 static double* mapped(void* h) {
-  if (!h) return nullptr;
+  if (!h || (reinterpret_cast<uintptr_t>(h) & 7)) return nullptr;
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
     cudaGetLastError();
