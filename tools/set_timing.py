@@ -20,7 +20,10 @@ from paper_2510_12897_b200.workloads import algorithmic_bytes_mode, build_worklo
 
 name = sys.argv[1] if len(sys.argv) > 1 else "case13659"
 mode = sys.argv[2] if len(sys.argv) > 2 else "set"
-model = build_workload(name, lower_to_gpu=False)
+# EXA_SHARD=r/N: rank r's shard of an N-way split of a batched config
+_shard = os.environ.get("EXA_SHARD")
+_r, _n = (int(v) for v in _shard.split("/")) if _shard else (0, 1)
+model = build_workload(name, lower_to_gpu=False, rank=_r, world=_n)
 bps = model_summary(model)["bytes_per_set"]
 mode_bytes = algorithmic_bytes_mode(model, mode)  # this callback's own compulsory bytes
 R = int(os.environ.get("EXA_R", "0")) or max(3, int(np.ceil(2 * 126 * 2**20 / mode_bytes)))
