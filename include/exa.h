@@ -218,7 +218,22 @@ int exa_pattern_create(ExaPlan* plan, int64_t n_raw, int64_t nnz, const int64_t*
  * plan whose kernels write those values. */
 int exa_pattern_create_known(ExaPlan* plan, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
                              const uint8_t* known, const double* known_val, ExaPattern** out);
+/* The Jacobian pattern for the compressed-set kernels (exa_plan_attach_compressed):
+ * direct[r] != 0 flags raw slot r as written straight into its compressed
+ * entry by the set kernel (0.0 + value, np.bincount's single-slot fold; the
+ * entry must have exactly that one raw slot) -- those entries are left out
+ * of the segmented sum.  Used by exa_eval_set_compressed only on a plan with
+ * the compressed-set module attached. */
+int exa_pattern_create_direct(ExaPlan* plan, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
+                              const uint8_t* known, const double* known_val, const uint8_t* direct,
+                              ExaPattern** out);
 void exa_pattern_destroy(ExaPattern* pattern);
+/* Attach the compressed-set module of a plan: a cubin (exa_jit_compile) with
+ * set kernels exa_k_setc_h / exa_k_setc_l that write the direct compressed
+ * Jacobian entries (ExaArgs.Jc) and keep every other raw slot in L2 for the
+ * segmented sum.  Built host-side from the same layout as the plan's module
+ * plus the direct entries' positions (paper_2510_12897_b200.device). */
+int exa_plan_attach_compressed(ExaPlan* plan, const void* cubin, int64_t cubin_size);
 /* cons + COMPRESSED Jacobian and Hessian values of one point: the set kernel
  * writes the raw slots into the workspace's scratch and the two segmented
  * sums run in one programmatic-dependent launch behind it (reference

@@ -395,7 +395,13 @@ class CompressedPattern:
         Every plan of one model with the same zero-sign mode has the same
         runs, so the handle is shared by them."""
         handles = self.__dict__.setdefault("_exa_handles", {})
-        key = (dp.device, kind, bool(dp.exact_zero_sign) if kind else None)
+        # the plan's compressed-set kernels write the Jacobian entries of
+        # whole-row term blocks themselves (DevicePlan.jac_direct_mask, which
+        # also attaches those kernels to dp): such a pattern serves only plans
+        # with the same direct blocks
+        direct = dp.jac_direct_mask(self) if kind == "jac" else None
+        dsig = tuple(sorted(dp.layout.jdirect)) if direct is not None else None
+        key = (dp.device, kind, bool(dp.exact_zero_sign) if kind else None, dsig)
         h = handles.get(key)
         if h is None:
             order = np.argsort(self.slot_map, kind="stable")
@@ -414,10 +420,16 @@ class CompressedPattern:
                 for a, n, bits in runs:
                     known[a:a + n] = 1
                     val[a:a + n] = bits
-                _lib.check(dp._lib.exa_pattern_create_known(dp.handle, int(self.slot_map.size), self.nnz,
-                                                            ptr.ctypes.data, ent.ctypes.data, known.ctypes.data,
-                                                            val.ctypes.data, C.byref(h)),
-                           "exa_pattern_create_known")
+                if direct is not None:
+                    _lib.check(dp._lib.exa_pattern_create_direct(
+                        dp.handle, int(self.slot_map.size), self.nnz, ptr.ctypes.data, ent.ctypes.data,
+                        known.ctypes.data, val.ctypes.data, direct.ctypes.data, C.byref(h)),
+                        "exa_pattern_create_direct")
+                else:
+                    _lib.check(dp._lib.exa_pattern_create_known(dp.handle, int(self.slot_map.size), self.nnz,
+                                                                ptr.ctypes.data, ent.ctypes.data, known.ctypes.data,
+                                                                val.ctypes.data, C.byref(h)),
+                               "exa_pattern_create_known")
             handles[key] = h
         return h
 

@@ -785,8 +785,17 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
         g.deriv = relax
         adj = pc._adjoints(g, v)
         grads = pc._slot_sums(g, adj)
+        jc0 = mem.get("jc0")  # compressed-set module: this member's J entries are direct
         for s_ in range(k):
             dst = early if const(grads[s_]) else g.lines
+            if jc0 is not None:
+                # compressed J: the record's row holds exactly its k slots, in
+                # column order -> entry jc0 + k r + rank of the slot's column;
+                # value 0.0 + v (np.bincount's single-slot fold)
+                rank = " + ".join(f"({cnames[m][t_]} < {cnames[m][s_]})" for t_ in range(k) if t_ != s_) or "0"
+                dst.append(f"  if (MODE & EXA_M_JAC) __stcs(A.Jc + ({int(jc0)}LL + {k}LL * r + ({rank})), "
+                           f"0.0 + {R(grads[s_])});")
+                continue
             dst.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
             dst.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
         for seed in range(k):

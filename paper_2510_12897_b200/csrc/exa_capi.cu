@@ -137,6 +137,11 @@ struct ExaPlan {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern[EXA_NKERN] = {};
   cudaKernel_t kern_batch = nullptr; /* strided-batch set kernel (parameters kept in L2), if the module has one */
+  /* compressed-set module (exa_plan_attach_compressed): set kernels that write
+     the direct compressed Jacobian entries themselves and keep the other raw
+     slots in L2 for the segmented sum */
+  cudaLibrary_t lib_cmp = nullptr;
+  cudaKernel_t kern_cmp[2] = {};
   ExaWorkspace* dflt = nullptr;
   size_t bytes = 0;
   int pdl = 0;
@@ -170,6 +175,9 @@ struct ExaPlan {
 struct ExaPattern {
   int device = 0;
   int64_t n_raw = 0, nnz = 0;
+  /* entries written directly by the compressed-set kernels (their single raw
+     slot is flagged direct at creation): not folded here */
+  bool direct = false;
   /* CTA chunks of the compressed sum.  Each entry's raw slots, in increasing
      slot order, minus the slots known to hold +0.0 on every call (dropping
      them from a fold that starts at +0.0 is exact), form its *stage*; chunk b
@@ -840,6 +848,7 @@ void exa_plan_destroy(ExaPlan* p) {
   cudaFree(p->grad_ptr);
   cudaFree(p->grad_ent);
   cudaFree(p->d2h);
+  if (p->lib_cmp) cudaLibraryUnload(p->lib_cmp);
   if (p->lib) cudaLibraryUnload(p->lib);
   delete p;
 }
@@ -1111,7 +1120,8 @@ int exa_plan_info(const ExaPlan* p, int64_t* bytes, int32_t* regs) {
   return 0;
 }
 
-static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStream_t st, unsigned nbatch = 1) {
+static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStream_t st, unsigned nbatch = 1,
+                      bool cmp = false) {
   const ExaTerm* terms = p->terms;
   const ExaSeg* segs = p->segs[kid];
   const int* cmap = p->cta_seg[kid];
@@ -1130,13 +1140,16 @@ static int launch_kid(ExaPlan* p, ExaWorkspace* w, int kid, ExaArgs A, cudaStrea
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool batch_kernel = nbatch > 1 && kid == 2 * EXA_MODE_SET + 1 && p->kern_batch;
-  CU(cudaLaunchKernelExC(&cfg, (const void*)(batch_kernel ? p->kern_batch : p->kern[kid]), args));
+  cudaKernel_t k = batch_kernel ? p->kern_batch : p->kern[kid];
+  if (cmp) k = p->kern_cmp[kid & 1];
+  CU(cudaLaunchKernelExC(&cfg, (const void*)k, args));
   return 0;
 }
 
 // One callback = its heavy kernel on `st` and its light kernel on the
 // workspace's aux stream, forked/joined with events (graph-capturable).
-static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaStream_t st, unsigned nbatch = 1) {
+static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaStream_t st, unsigned nbatch = 1,
+                       bool cmp = false) {
   A.err = w->err;
   A.trace = g_trace;
   A.obj_base = p->err_base[mode][0];
@@ -1151,14 +1164,14 @@ static int launch_mode(ExaPlan* p, ExaWorkspace* w, int mode, ExaArgs& A, cudaSt
     // light kernel's many short CTAs fill every SM
     CU(cudaEventRecord(w->fork, st));
     CU(cudaStreamWaitEvent(w->aux, w->fork, 0));
-    if ((rc = launch_kid(p, w, kh, A, st, nbatch))) return rc;
-    if ((rc = launch_kid(p, w, kl, A, w->aux, nbatch))) return rc;
+    if ((rc = launch_kid(p, w, kh, A, st, nbatch, cmp))) return rc;
+    if ((rc = launch_kid(p, w, kl, A, w->aux, nbatch, cmp))) return rc;
     CU(cudaEventRecord(w->join, w->aux));
     CU(cudaStreamWaitEvent(st, w->join, 0));
   } else if (h) {
-    rc = launch_kid(p, w, kh, A, st, nbatch);
+    rc = launch_kid(p, w, kh, A, st, nbatch, cmp);
   } else if (l) {
-    rc = launch_kid(p, w, kl, A, st, nbatch);
+    rc = launch_kid(p, w, kl, A, st, nbatch, cmp);
   }
   return rc;
 }
@@ -1191,8 +1204,8 @@ struct DeviceGuard {
   memset(&A, 0, sizeof A);                                  \
   if (int rc_ = reset_err(p, w, st)) return rc_;
 
-int exa_eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
-                 double* jac, double* hess, exa_stream_t stream) {
+static int eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
+                    double* jac, double* hess, exa_stream_t stream, double* jac_c) {
   EXA_PROLOGUE();
   A.x = x;
   A.y = mult;
@@ -1200,7 +1213,13 @@ int exa_eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mu
   A.c = c;
   A.J = jac;
   A.H = hess;
-  return launch_mode(p, w, EXA_MODE_SET, A, st);
+  A.Jc = jac_c;
+  return launch_mode(p, w, EXA_MODE_SET, A, st, 1, jac_c != nullptr);
+}
+
+int exa_eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
+                 double* jac, double* hess, exa_stream_t stream) {
+  return eval_set(p, ws, x, mult, w_obj, c, jac, hess, stream, nullptr);
 }
 
 int exa_eval_set_batch(ExaPlan* p, ExaWorkspace* ws, int64_t nsets, const double* x, const double* mult,
@@ -1535,7 +1554,8 @@ int exa_eval_hess_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const doub
 }
 
 static int pattern_build(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
-                         const uint8_t* known, const double* known_val, ExaPattern** out) {
+                         const uint8_t* known, const double* known_val, ExaPattern** out,
+                         const uint8_t* direct = nullptr) {
   if (!p || !out || n_raw < 0 || nnz < 0 || (nnz && !ptr) || (n_raw && !ent) || (known && !known_val))
     return fail("exa_pattern_create: invalid argument");
   *out = nullptr;
@@ -1562,18 +1582,33 @@ static int pattern_build(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* 
   /* chunks of consecutive entries (ordering the entries by the record that
      produces their slots, so that gathers become runs, measured slower:
      case13659 18.0 vs 18.2 us, MP96 149 vs 131 us) */
-  std::vector<int32_t> order((size_t)nnz);
-  for (int64_t k = 0; k < nnz; ++k) order[k] = (int32_t)k;
-  std::vector<int32_t> chk{0}, che{0}, chc{0}, src, eout((size_t)nnz);
+  // entries written directly by the compressed-set kernels: exactly one raw
+  // slot, flagged direct; they are left out of the chunks
+  std::vector<int32_t> order;
+  order.reserve((size_t)nnz);
+  for (int64_t k = 0; k < nnz; ++k) {
+    bool dir = false;
+    if (direct)
+      for (int64_t e = ptr[k]; e < ptr[k + 1]; ++e)
+        if (direct[ent[e]]) {
+          if (ptr[k + 1] - ptr[k] != 1)
+            return fail("exa_pattern_create_direct: entry %lld has a direct slot among %lld slots", (long long)k,
+                        (long long)(ptr[k + 1] - ptr[k]));
+          dir = true;
+        }
+    if (!dir) order.push_back((int32_t)k);
+  }
+  const int64_t n_fold = (int64_t)order.size();
+  std::vector<int32_t> chk{0}, che{0}, chc{0}, src, eout((size_t)n_fold);
   std::vector<uint16_t> dst, cpos, cid;
-  std::vector<uint32_t> edesc((size_t)nnz);
-  std::vector<int32_t> est((size_t)nnz);
+  std::vector<uint32_t> edesc((size_t)n_fold);
+  std::vector<int32_t> est((size_t)n_fold);
   std::vector<double> cval;
   std::unordered_map<uint64_t, uint16_t> cmap;
   std::vector<std::pair<int32_t, int32_t>> gat;
-  for (int64_t q0 = 0; q0 < nnz;) {
+  for (int64_t q0 = 0; q0 < n_fold;) {
     int64_t q1 = q0 + 1, tot = stage_len[order[q0]];
-    while (q1 < nnz && q1 - q0 < EXA_CMP_CAP && tot + stage_len[order[q1]] <= EXA_CMP_CAP) tot += stage_len[order[q1++]];
+    while (q1 < n_fold && q1 - q0 < EXA_CMP_CAP && tot + stage_len[order[q1]] <= EXA_CMP_CAP) tot += stage_len[order[q1++]];
     if (tot > EXA_CMP_CAP) {  // one long entry: every non-dropped slot gathered, slot order
       const int64_t k = order[q0];
       for (int64_t e = ptr[k]; e < ptr[k + 1]; ++e)
@@ -1637,6 +1672,7 @@ static int pattern_build(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* 
   q->device = p->device;
   q->n_raw = n_raw;
   q->nnz = nnz;
+  q->direct = direct != nullptr;
   q->nch = (int32_t)(chk.size() - 1);
   q->ipt = ipt;
   int rc = dev_upload(&q->chk, chk.data(), chk.size());
@@ -1660,6 +1696,32 @@ static int pattern_build(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* 
 int exa_pattern_create_known(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
                              const uint8_t* known, const double* known_val, ExaPattern** out) {
   return pattern_build(p, n_raw, nnz, ptr, ent, known, known_val, out);
+}
+
+int exa_pattern_create_direct(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
+                              const uint8_t* known, const double* known_val, const uint8_t* direct,
+                              ExaPattern** out) {
+  if (!direct) return fail("exa_pattern_create_direct: null direct mask");
+  return pattern_build(p, n_raw, nnz, ptr, ent, known, known_val, out, direct);
+}
+
+int exa_plan_attach_compressed(ExaPlan* p, const void* cubin, int64_t cubin_size) {
+  if (!p || !cubin || cubin_size <= 0) return fail("exa_plan_attach_compressed: invalid argument");
+  if (p->lib_cmp) return 0;  // attached once per plan
+  DeviceGuard g(p->device);
+  cudaLibrary_t lib = nullptr;
+  cudaError_t e = cudaLibraryLoadData(&lib, cubin, nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e != cudaSuccess) return fail("cudaLibraryLoadData (compressed module): %s", cudaGetErrorString(e));
+  cudaKernel_t k[2];
+  for (int h = 0; h < 2; ++h)
+    if ((e = cudaLibraryGetKernel(&k[h], lib, h ? "exa_k_setc_l" : "exa_k_setc_h")) != cudaSuccess) {
+      cudaLibraryUnload(lib);
+      return fail("cudaLibraryGetKernel(exa_k_setc_%s): %s", h ? "l" : "h", cudaGetErrorString(e));
+    }
+  p->kern_cmp[0] = k[0];
+  p->kern_cmp[1] = k[1];
+  p->lib_cmp = lib;
+  return 0;
 }
 
 int exa_pattern_create(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
@@ -1694,7 +1756,12 @@ static int set_compressed(ExaPlan* p, ExaWorkspace* w, const ExaPattern* jp, con
   if (jp && hp && jp->ipt != hp->ipt) return fail("exa_eval_set_compressed: patterns chunked for different EXA_CMP_IPT");
   double* rawJ = jp ? w->dJ : jc;
   double* rawH = hp ? w->dH : hc;
-  int rc = exa_eval_set(p, w, x, mult, w_obj, c, rawJ, rawH, st);
+  if (jp && jp->direct && !(p->kern_cmp[0] && p->kern_cmp[1]))
+    return fail("exa_eval_set_compressed: direct Jacobian pattern but no compressed-set module attached");
+  if (hp && hp->direct) return fail("exa_eval_set_compressed: direct Hessian patterns are not supported");
+  // direct J pattern: the compressed-set kernels write the direct entries into
+  // jc themselves and every other raw slot into the workspace scratch
+  int rc = eval_set(p, w, x, mult, w_obj, c, rawJ, rawH, (exa_stream_t)st, jp && jp->direct ? jc : nullptr);
   if (rc) return rc;
   const int nchJ = jp ? jp->nch : 0, nchH = hp ? hp->nch : 0;
   if (nchJ + nchH == 0) return 0;

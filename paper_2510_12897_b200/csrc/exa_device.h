@@ -74,6 +74,7 @@ typedef struct ExaArgs {
   const double* f64; /* plan blobs (model-specialised modules address terms */
   const int* i32;    /*   as blob + compile-time offsets)                    */
   long long* trace;  /* diagnostics timeline (EXA_TRACE modules), else 0 */
+  double* Jc;        /* compressed Jacobian (compressed-set kernels: direct entries) */
 } ExaArgs;
 
 /* domain-error key: order (20 bits) | instr (12 bits) | record+1 (32 bits) */

@@ -544,6 +544,50 @@ class HostLayout:
         self.source = module_source(self.patterns, layout=self if self.specialised else None,
                                     threads=self.threads[1])
 
+    def jac_direct(self, jp):
+        """Term-group members whose Jacobian entries the compressed-set
+        kernels write directly: ({term: jc0}, uint8 mask of their raw J slots).
+
+        A member is direct when every one of its records' rows holds exactly
+        that record's k slots, one raw slot per compressed entry, with
+        distinct columns: the row's entries are then its slots in column
+        order, and slot s of record r lands at ``jc0 + k r + rank`` (rank = how
+        many of the record's other columns are smaller), ``jc0`` = the row
+        block's first entry in ``jp`` (np.unique order of
+        ``compress_coordinates``, reference autodiff.py:677-689).  OPF: the
+        four flow blocks, thermal limits and angle differences -- every
+        Jacobian row but the bus balances.  The result is kept on the layout
+        (``jdirect``) for :meth:`compressed_source`."""
+        jdir, mask = {}, np.zeros(jp.slot_map.size, dtype=np.uint8)
+        if jp.nnz:
+            counts = np.bincount(jp.slot_map, minlength=jp.nnz)
+            for t in sorted(self.group_of):
+                tp = self.terms[t]
+                k, n = tp.tape.k, tp.nrec
+                if tp.kind != "constraint" or tp.row_offset is None or not k or not n:
+                    continue
+                raw = np.stack([np.arange(lo, lo + n, dtype=np.int64) for lo, _ in tp.jac_slices[:k]])
+                e = jp.slot_map[raw]
+                if not np.all(counts[e] == 1):
+                    continue
+                cols = np.stack([np.asarray(c, dtype=np.int64) for c in tp.cols[:k]])
+                srt = np.sort(cols, axis=0)
+                if k > 1 and np.any(srt[1:] == srt[:-1]):
+                    continue
+                rank = (cols[None, :, :] < cols[:, None, :]).sum(axis=1)
+                jc0 = int(np.searchsorted(jp.rows, tp.row_offset))
+                if not np.array_equal(e, jc0 + k * np.arange(n, dtype=np.int64)[None, :] + rank):
+                    continue
+                jdir[t] = jc0
+                mask[raw.ravel()] = 1
+        self.jdirect = jdir
+        return jdir, mask
+
+    def compressed_source(self) -> str:
+        """CUDA source of the compressed-set module (set kernels
+        ``exa_k_setc_h`` / ``_l``; needs :meth:`jac_direct` first)."""
+        return module_source(self.patterns, layout=self, threads=self.threads[1], compressed=True)
+
     def _locality_order(self, terms, period: int):
         """Real CTA -> virtual CTA of the set kernel (light half): virtual CTAs
         sorted by (instance window of their first record, virtual index).  A
@@ -920,6 +964,30 @@ class DevicePlan:
         self._tls = threading.local()
         self._ws_lock = threading.Lock()
         self._workspaces: list = []
+
+    def jac_direct_mask(self, jp):
+        """Raw Jacobian slots the compressed-set kernels write straight into
+        their compressed entries (``HostLayout.jac_direct``), after compiling
+        and attaching the plan's compressed-set module; None for generic
+        modules, no eligible term, or ``EXA_JDIRECT=0``."""
+        if hasattr(self, "_jdirect_mask"):
+            return self._jdirect_mask
+        self._jdirect_mask = None
+        lay = self.layout
+        if not lay.specialised or os.environ.get("EXA_JDIRECT", "1") != "1":
+            return None
+        jdir, mask = lay.jac_direct(jp)
+        if not jdir:
+            return None
+        cubin = compile_module(lay.compressed_source())
+        buf = C.create_string_buffer(cubin, len(cubin))
+        import torch
+
+        with torch.cuda.device(self.device):
+            _lib.check(self._lib.exa_plan_attach_compressed(self.handle, C.cast(buf, C.c_void_p), len(cubin)),
+                       "exa_plan_attach_compressed")
+        self._jdirect_mask = mask
+        return mask
 
     def workspace(self) -> C.c_void_p:
         """The calling thread's workspace (objective / gradient scratch,

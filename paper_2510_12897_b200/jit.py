@@ -87,7 +87,8 @@ _LD_RES = (re.compile(r"__ldg\((T\d*\.(?:f|ix)\[[^\]]*\] \+ (?:r|o))\)"),
            re.compile(r"__ldg\((reinterpret_cast<const int2\*>\(A\.i32 \+ \d+LL\) \+ [^;]*?)\)(?=;)"),
            re.compile(r"__ldg\((A\.i32 \+ \d+LL \+ q)\)"),
            re.compile(r"__ldg\(((?:T\d*|U\d+)\.rows \+ [^)]*)\)"))
-_ST_RE = re.compile(r"\b(Jout|Hout|Cout|A\.c)\[([^\]\[]*)\] = ([^;]*);")  # release point inside term groups (see EXA_GRID_RELEASE_MID)
+_ST_RE = re.compile(r"\b(Cout|A\.c)\[([^\]\[]*)\] = ([^;]*);")
+_ST_JH_RE = re.compile(r"\b(Jout|Hout)\[([^\]\[]*)\] = ([^;]*);")  # release point inside term groups (see EXA_GRID_RELEASE_MID)
 
 _lock = threading.Lock()
 _mem_cache: dict = {}
@@ -187,8 +188,12 @@ _PREFETCH = r"""
 // launch evaluates one set; the strided-batch kernel (LDH = 0) reads the same
 // parameters for every set of the launch, so there they stay in L2.  LDH is a
 // template parameter of the generated functions; this is the default outside.
+// Bit 2 of LDH (compressed-set kernels, exa_k_setc_*) keeps the raw J / H
+// slots in L2 (plain instead of evict-first stores): the segmented sum reads
+// them right back and the next set overwrites the workspace scratch.
 constexpr int LDH = 1;
-#define EXA_LDP(p) (LDH ? __ldcs(p) : __ldg(p))
+#define EXA_LDP(p) ((LDH & 1) ? __ldcs(p) : __ldg(p))
+#define EXA_STO(p, v) do { if (LDH & 2) *(p) = (v); else __stcs((p), (v)); } while (0)
 // Bulk L2 prefetch of the gathered inputs: CTA b < n prefetches chunk b of x
 // (then of y).  The first random gathers of a set would otherwise miss L2
 // (the previous set used other buffers) and go to DRAM one 32-B sector at a
@@ -321,7 +326,7 @@ _MODE_BITS = ("EXA_M_CONS | EXA_M_JAC | EXA_M_HESS", "EXA_M_CONS", "EXA_M_JAC", 
               "EXA_M_OBJV", "EXA_M_GRAD")
 
 
-def _specialised_kernels(layout) -> str:
+def _specialised_kernels(layout, compressed: bool = False) -> str:
     """Kernel bodies with the model's metadata as compile-time constants.
 
     Every term becomes an ``exa_init_T<t>`` that fills a local ExaTerm from
@@ -383,7 +388,7 @@ def _specialised_kernels(layout) -> str:
             oc.append(f"{lab} exa_termx_{layout.term_pid[u]}(xv, w, jv, hv); j0 = {descs[u]['jac0']}LL;"
                       f" h0 = {descs[u]['hess0']}LL; break;")
         ocases = "\n".join(oc)
-        out.append(f"""template <int WJ, int WH>
+        out.append(f"""template <int WJ, int WH, int LDH = 1>
 __device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, const double w, const int rec, const ExaArgs& A) {{
   double jv, hv;
   long long j0, h0;
@@ -395,14 +400,21 @@ __device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, con
   if (WJ) Jout[j0 + rec] = jv;
   if (WH) Hout[h0 + rec] = hv;
 }}""")
+    jdir = getattr(layout, "jdirect", {}) if compressed else {}
     for gid, (pid, grp, members) in enumerate(getattr(layout, "groups", [])):
         augs = [(layout.patterns[layout.term_pid[u]], off, m, s_)
                 for (u, off, m, s_) in getattr(layout, "group_augs", {}).get(gid, [])]
-        out.append(group_source(gid, [(layout.patterns[layout.term_pid[u]], mem) for u, mem in zip(grp, members)],
+        out.append(group_source(gid, [(layout.patterns[layout.term_pid[u]],
+                                       dict(mem, jc0=jdir[u]) if u in jdir else mem)
+                                      for u, mem in zip(grp, members)],
                                 augs, relax=layout.relax))
-    for m, name in enumerate(KERNEL_NAMES):
+    if compressed:  # the compressed-set module: set kernels only
         for half, suffix in ((0, "_h"), (1, "_l")):
-            out.append(_kernel_source(layout, m, half, name + suffix))
+            out.append(_kernel_source(layout, 0, half, "exa_k_setc" + suffix, ldh=3))
+    else:
+        for m, name in enumerate(KERNEL_NAMES):
+            for half, suffix in ((0, "_h"), (1, "_l")):
+                out.append(_kernel_source(layout, m, half, name + suffix))
     return _cache_hints("\n\n".join(out))
 
 
@@ -420,6 +432,7 @@ def _cache_hints(src: str) -> str:
     x and y keep ``__ldg`` (gathered, reused across records)."""
     if ST_CS:
         src = _ST_RE.sub(r"__stcs(&\1[\2], \3);", src)
+        src = _ST_JH_RE.sub(r"EXA_STO(&\1[\2], \3);", src)
     if LD_CS:
         for pat in _LD_RES:
             src = pat.sub(r"EXA_LDP(\1)", src)
@@ -473,7 +486,7 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, m):
     if want_v:
         L.append(f"      v = exa_bkval_T{t}(e, xv);")
     if want_j or want_h:
-        L.append(f"      if (e >= 0 && rc >= 0) exa_bkout_T{t}<{int(want_j)}, {int(want_h)}>(e, xv, wrow, rc, A);")
+        L.append(f"      if (e >= 0 && rc >= 0) exa_bkout_T{t}<{int(want_j)}, {int(want_h)}, LDH>(e, xv, wrow, rc, A);")
     L.append("    }")
     if want_v:
         if LW == 32:
@@ -493,7 +506,7 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, m):
     return L
 
 
-def _kernel_source(layout, m, half, kname) -> str:
+def _kernel_source(layout, m, half, kname, ldh: int = 1) -> str:
     """One entry kernel of a specialised module.
 
     ``exa_vb_<kname>(b, tid, A)`` evaluates virtual CTA ``b`` (the segment
@@ -580,7 +593,7 @@ def _kernel_source(layout, m, half, kname) -> str:
                             b_.append(f"    acc = e{k} >= 0 ? acc + v{k} : acc;")
                     if want_j or want_h:
                         cond = f"if (rc{k} >= 0) " if k < always else f"if (e{k} >= 0 && rc{k} >= 0) "
-                        b_.append(f"    {cond}exa_bkout_T{t}<{int(want_j)}, {int(want_h)}>(e{k}, xv{k}, wrow, rc{k}, A);")
+                        b_.append(f"    {cond}exa_bkout_T{t}<{int(want_j)}, {int(want_h)}, LDH>(e{k}, xv{k}, wrow, rc{k}, A);")
             if want_v:
                 b_.append("    A.c[T.row_offset + r] = acc;")
             b_.append("    return;")
@@ -664,8 +677,8 @@ def _kernel_source(layout, m, half, kname) -> str:
     body.append("  EXA_GRID_RELEASE();")
     body.append("}")
     entry = "\n".join(body)
-    out = "\n".join(fn_body) + "\n" + entry.replace("@LDH@", "1")
-    if m == 0 and half == 1:  # strided-batch entry (exa_eval_set_batch): parameters stay in L2
+    out = "\n".join(fn_body) + "\n" + entry.replace("@LDH@", str(ldh))
+    if m == 0 and half == 1 and ldh == 1:  # strided-batch entry (exa_eval_set_batch): parameters stay in L2
         out += "\n" + entry.replace("@LDH@", "0").replace(f" {kname}(", f" {kname.replace('_set_', '_setb_')}(", 1)
     return out
 
@@ -673,7 +686,7 @@ def _kernel_source(layout, m, half, kname) -> str:
 KERNEL_NAMES = ("exa_k_set", "exa_k_cons", "exa_k_jac", "exa_k_hess", "exa_k_objv", "exa_k_grad")
 
 
-def module_source(patterns, layout=None, threads: int = 32) -> str:
+def module_source(patterns, layout=None, threads: int = 32, compressed: bool = False) -> str:
     """CUDA source of a model's module.
 
     ``layout`` given -> *model-specialised* module: term metadata and the
@@ -704,7 +717,7 @@ def module_source(patterns, layout=None, threads: int = 32) -> str:
         parts.append(_KERNELS_GENERIC)
         parts.append(_ENTRIES)
     else:
-        parts.append(_specialised_kernels(layout))
+        parts.append(_specialised_kernels(layout, compressed))
     bl = f"{threads}, {min_blocks(threads)}"
     return "\n".join(parts).replace("@BOUNDS_L@", bl).replace("@BOUNDS_H@", str(THREADS_HEAVY))
 

@@ -30,6 +30,12 @@ R = int(os.environ.get("EXA_R", "0")) or max(3, int(np.ceil(2 * 126 * 2**20 / mo
 dev = torch.device("cuda", 0)
 t0 = time.time()
 plans = [DevicePlan(model, 0) for _ in range(R)]
+if os.environ.get("EXA_ATTACH_CMP") == "1":  # diagnostics: plans with the compressed-set module attached
+    from paper_2510_12897_b200 import model_patterns
+
+    _jp = model_patterns(model)[0]
+    for _p in plans:
+        _p.jac_direct_mask(_jp)
 tjit = time.time() - t0
 lib = _lib.load()
 bufs = []
