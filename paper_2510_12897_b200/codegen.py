@@ -47,6 +47,22 @@ def _zero_const(v) -> bool:
     return float(v.value if isinstance(v, Arr) else v) == 0.0
 
 
+def _field_load(T: str, fi: int, r: str) -> str:
+    """Field fi of term T at record r.  Periodic columns (``T.fmask`` bit fi,
+    batched element-major models) hold one value per element; the selection
+    folds at compile time in model-specialised modules (T is built from
+    literals).  The per-record form stays an evict-first candidate
+    (jit._cache_hints rewrites ``__ldg(T.f[..] + r)``)."""
+    return f"((({T}.fmask >> {fi}) & 1u) ? __ldg({T}.f[{fi}] + {r} / {T}.per) : __ldg({T}.f[{fi}] + {r}))"
+
+
+def _index_load(T: str, c: int, r: str) -> str:
+    """Index column c of term T at record r (periodic columns: the element's
+    t = 0 position + r % per)."""
+    return (f"((({T}.imask >> {c}) & 1u) ? __ldg({T}.ix[{c}] + {r} / {T}.per) + {r} % {T}.per"
+            f" : __ldg({T}.ix[{c}] + {r}))")
+
+
 # Zero-sign mode of the generated code.  Exact: every 0 + x of the reference
 # and the structural zeros w * 0 with their weight's sign (bit-identical J/H,
 # NaN / inf multipliers propagate like the reference's).  Relaxed: the former
@@ -547,10 +563,10 @@ class PatternCode:
         loads = {"field": {}, "var": []}
         pre = []
         for fi, fname in enumerate(self.tape.field_names):
-            pre.append(f"  const double f{fi} = __ldg(T.f[{fi}] + r);")
+            pre.append(f"  const double f{fi} = {_field_load('T', fi, 'r')};")
             loads["field"][fname] = Sym(f"f{fi}")
         for ii in range(self.ni):
-            pre.append(f"  const int i{ii} = __ldg(T.ix[{ii}] + r);")
+            pre.append(f"  const int i{ii} = {_index_load('T', ii, 'r')};")
         pre_wait = len(pre)
         for s, (_, ic) in enumerate(self.slot_struct):
             pre.append(f"  const int c{s} = T.voff[{s}] + i{ic};")
@@ -731,12 +747,12 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
         for c, u in enumerate(mem["cols"]):
             u_src.setdefault(u, (m, c))
     for u, (m, c) in sorted(u_src.items()):
-        pre.append(f"  const int i{u} = __ldg(T{m}.ix[{c}] + r);")
+        pre.append(f"  const int i{u} = {_index_load(f'T{m}', c, 'r')};")
     fsyms = []
     for m, (pc, mem) in enumerate(entries):
         d = {}
         for fi, fname in enumerate(pc.tape.field_names):
-            pre.append(f"  const double f{m}_{fi} = __ldg(T{m}.f[{fi}] + r);")
+            pre.append(f"  const double f{m}_{fi} = {_field_load(f'T{m}', fi, 'r')};")
             d[fname] = Sym(f"f{m}_{fi}")
         fsyms.append(d)
     xkey: dict = {}

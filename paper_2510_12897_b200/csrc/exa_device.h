@@ -50,6 +50,14 @@ typedef struct ExaTerm {
   long long jac0;            /* first raw Jacobian slot (con terms)        */
   long long hess0;           /* first raw Hessian slot                     */
   long long scr0;            /* objective scratch: values / slot grads     */
+  /* periodic parameter columns (batched models, element-major records
+     r = e * per + t): field fi with bit fi of fmask is stored once per
+     element (read at r / per); index column c with bit c of imask holds the
+     element's t = 0 position (column value = ix[r / per] + r % per).
+     Specialised modules only; 0 elsewhere. */
+  int per;
+  unsigned int fmask, imask;
+  int pad2;
 } ExaTerm;
 
 typedef struct ExaSeg {

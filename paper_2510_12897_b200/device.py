@@ -65,6 +65,32 @@ HALF_ROWS = os.environ.get("EXA_HALF_ROWS", "1") == "1"  # long bucket rows of <
 # compiled in as constants); larger ones (e.g. thousands of per-instance
 # blocks) use the generic module with run-time term tables.
 META_CONST_MAX_TERMS = 80
+# periodic parameter columns of batched element-major models (plan.batch_period)
+PERIODIC = os.environ.get("EXA_PERIODIC", "1") == "1"
+
+
+def _periodic(tp, period):
+    """(per, fmask, imask) of a term whose records are element-major over
+    ``period`` (r = e * period + t): field columns constant within every
+    element's run are stored once per element (fmask), index columns that
+    step by one within every run are stored as the run's first position
+    (imask).  MP models: branch admittances, costs, limits and the (bus,
+    period) variable positions; loads vary per period and stay per record.
+    (0, 0, 0) when nothing reduces."""
+    n = tp.nrec
+    if not period or period < 2 or n == 0 or n % period:
+        return 0, 0, 0
+    fmask = imask = 0
+    for fi, nm in enumerate(tp.tape.field_names):
+        col = np.ascontiguousarray(tp.reals[nm], dtype=np.float64).view(np.int64).reshape(-1, period)
+        if np.all(col == col[:, :1]):
+            fmask |= 1 << fi
+    steps = np.arange(period, dtype=np.int64)[None, :]
+    for c, nm in enumerate(tp.tape.index_names):
+        col = np.asarray(tp.table.indices[nm], dtype=np.int64).reshape(-1, period) - steps
+        if np.all(col == col[:, :1]):
+            imask |= 1 << c
+    return (int(period) if (fmask or imask) else 0), fmask, imask
 
 # Run heavy patterns in a separate concurrent kernel (measured slower on
 # case13659: the fork/join costs more than the register specialisation wins).
@@ -317,11 +343,16 @@ class HostLayout:
         self.buckets: dict = {}
         scr = 0
         self.scr0 = []
+        period = getattr(plan, "batch_period", None) if (PERIODIC and self.specialised_ok) else None
         for t, tp in enumerate(terms):
+            per, fmask, imask = _periodic(tp, period)
             d = {
-                "f_off": [f64.add(tp.reals[nm]) for nm in tp.tape.field_names],
-                "ix_off": [i32.add(_i32(tp.table.indices[nm], f"index column {nm!r}"))
-                           for nm in tp.tape.index_names],
+                "f_off": [f64.add(np.asarray(tp.reals[nm])[::per] if (fmask >> fi) & 1 else tp.reals[nm])
+                          for fi, nm in enumerate(tp.tape.field_names)],
+                "ix_off": [i32.add(_i32(np.asarray(tp.table.indices[nm])[::per] if (imask >> c) & 1
+                                        else tp.table.indices[nm], f"index column {nm!r}"))
+                           for c, nm in enumerate(tp.tape.index_names)],
+                "per": per, "fmask": fmask, "imask": imask,
                 "voff": [blk.offset for blk in tp.slot_blocks],
                 "rows_off": i32.add(_i32(tp.rows, "augment rows")) if tp.kind == "augment" else -1,
                 "row_ptr_off": -1, "row_ent_off": -1,

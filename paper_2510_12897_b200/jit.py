@@ -350,6 +350,7 @@ def _specialised_kernels(layout, compressed: bool = False) -> str:
             lines.append(f"  T.{k} = {d[k]};")
         for k in ("jac0", "hess0", "scr0"):
             lines.append(f"  T.{k} = {d[k]}LL;")
+        lines.append(f"  T.per = {d.get('per', 0)}; T.fmask = {d.get('fmask', 0)}u; T.imask = {d.get('imask', 0)}u;")
         lines.append("}")
         out.append("\n".join(lines))
     # per augment-target block: value of any contributing (term, record)
@@ -460,6 +461,7 @@ def _warp_row_source(layout, t, bi, cta0, n_cta, threads, m):
         L.append(f"    T.f[{i}] = A.f64 + {off}LL;")
     for i, off in enumerate(bk["ix_off"]):
         L.append(f"    T.ix[{i}] = A.i32 + {off}LL;")
+    L.append("    T.fmask = 0u; T.imask = 0u;  // bucket-order copies are per row")
     LW = bk["d"]  # lanes per row: 32, or 16 (two rows per warp)
     if LW == 32:
         L += [f"    const int q = (b - {cta0}) * {threads // 32} + tid / 32;",
@@ -539,6 +541,7 @@ def _kernel_source(layout, m, half, kname, ldh: int = 1) -> str:
                 b_.append(f"    T.f[{i}] = A.f64 + {off}LL;")
             for i, off in enumerate(bk["ix_off"]):
                 b_.append(f"    T.ix[{i}] = A.i32 + {off}LL;")
+            b_.append("    T.fmask = 0u; T.imask = 0u;  // bucket-order copies are per row")
             b_.append(f"    const int q = (b - {cta0}) * {threads} + tid;")
             b_.append(f"    if (q >= {n}) return;")
             b_.append(f"    const int r = __ldg(A.i32 + {bk['rows_off']}LL + q);")

@@ -13,7 +13,9 @@ Configs:
 
 ``algorithmic_bytes`` is SURVEY §8(d)'s compulsory-traffic count for one
 callback set (cons + jac + hess): x and y once, every term parameter once
-(fp64 fields, int32 index columns, +1 int32 row column for augments), every
+(fp64 fields, int32 index columns, +1 int32 row column for augments) as the
+device layout stores it -- per record, or once per element for the periodic
+columns of element-major batched models (MP96: 43.2 -> 6.0 MB) -- every
 output once.  COO structure arrays are not re-read per set.
 """
 
@@ -75,12 +77,32 @@ def build_workload(name: str, lower_to_gpu: bool = True, seed: int = 1, rank: in
     raise KeyError(name)
 
 
+def _term_param_bytes(tp, period) -> int:
+    """Parameter bytes of one term as the device layout stores them: fp64
+    fields and int32 index columns per record (+ the augment row column),
+    except periodic columns of element-major batched models, stored once per
+    element (``device._periodic``: MP models' branch admittances, costs,
+    limits and (bus, period) variable positions)."""
+    from .device import _periodic
+
+    per, fmask, imask = _periodic(tp, period)
+    n = tp.nrec
+    b = sum(8 * (n // per if (fmask >> fi) & 1 else n) for fi in range(len(tp.tape.field_names)))
+    b += sum(4 * (n // per if (imask >> c) & 1 else n) for c in range(len(tp.tape.index_names)))
+    return b + (4 * n if tp.kind == "augment" else 0)
+
+
+def _layout_period(plan):
+    from .device import META_CONST_MAX_TERMS, PERIODIC
+
+    specialised = len(plan.obj_terms) + len(plan.con_terms) <= META_CONST_MAX_TERMS
+    return getattr(plan, "batch_period", None) if (PERIODIC and specialised) else None
+
+
 def algorithmic_bytes(model) -> dict:
     plan = model.plan
-    params = 0
-    for tp in plan.obj_terms + plan.con_terms:
-        n_idx = len(tp.tape.index_names) + (1 if tp.kind == "augment" else 0)
-        params += tp.nrec * (8 * len(tp.tape.field_names) + 4 * n_idx)
+    period = _layout_period(plan)
+    params = sum(_term_param_bytes(tp, period) for tp in plan.obj_terms + plan.con_terms)
     parts = {
         "x": 8 * model.nvar,
         "y": 8 * model.ncon,
@@ -103,12 +125,10 @@ def algorithmic_bytes_mode(model, mode: str) -> int:
         return algorithmic_bytes(model)["total"]
     plan = model.plan
 
+    period = _layout_period(plan)
+
     def params(terms):
-        n = 0
-        for tp in terms:
-            n_idx = len(tp.tape.index_names) + (1 if tp.kind == "augment" else 0)
-            n += tp.nrec * (8 * len(tp.tape.field_names) + 4 * n_idx)
-        return n
+        return sum(_term_param_bytes(tp, period) for tp in terms)
 
     b = 8 * model.nvar
     if mode == "cons":
