@@ -47,19 +47,30 @@ def _zero_const(v) -> bool:
     return float(v.value if isinstance(v, Arr) else v) == 0.0
 
 
+def _elem(T: str, r: str) -> str:
+    """Element (per-element table row) of record r: r / per, or the key index
+    column's block position / per - g0 (device._periodic)."""
+    return f"({T}.kcol < 0 ? {r} / {T}.per : __ldg({T}.ix[{T}.kcol] + {r}) / {T}.per - {T}.g0)"
+
+
+def _inst(T: str, r: str) -> str:
+    """Instance / period of record r within its element."""
+    return f"({T}.kcol < 0 ? {r} % {T}.per : __ldg({T}.ix[{T}.kcol] + {r}) % {T}.per)"
+
+
 def _field_load(T: str, fi: int, r: str) -> str:
-    """Field fi of term T at record r.  Periodic columns (``T.fmask`` bit fi,
-    batched element-major models) hold one value per element; the selection
-    folds at compile time in model-specialised modules (T is built from
-    literals).  The per-record form stays an evict-first candidate
+    """Field fi of term T at record r.  Per-element columns (``T.fmask`` bit
+    fi, batched element-major models) are read at the record's element; the
+    selection folds at compile time in model-specialised modules (T is built
+    from literals).  The per-record form stays an evict-first candidate
     (jit._cache_hints rewrites ``__ldg(T.f[..] + r)``)."""
-    return f"((({T}.fmask >> {fi}) & 1u) ? __ldg({T}.f[{fi}] + {r} / {T}.per) : __ldg({T}.f[{fi}] + {r}))"
+    return f"((({T}.fmask >> {fi}) & 1u) ? __ldg({T}.f[{fi}] + {_elem(T, r)}) : __ldg({T}.f[{fi}] + {r}))"
 
 
 def _index_load(T: str, c: int, r: str) -> str:
-    """Index column c of term T at record r (periodic columns: the element's
-    t = 0 position + r % per)."""
-    return (f"((({T}.imask >> {c}) & 1u) ? __ldg({T}.ix[{c}] + {r} / {T}.per) + {r} % {T}.per"
+    """Index column c of term T at record r (per-element columns: the
+    element's g(e) * per + the record's instance)."""
+    return (f"((({T}.imask >> {c}) & 1u) ? __ldg({T}.ix[{c}] + {_elem(T, r)}) + {_inst(T, r)}"
             f" : __ldg({T}.ix[{c}] + {r}))")
 
 

@@ -50,13 +50,16 @@ typedef struct ExaTerm {
   long long jac0;            /* first raw Jacobian slot (con terms)        */
   long long hess0;           /* first raw Hessian slot                     */
   long long scr0;            /* objective scratch: values / slot grads     */
-  /* periodic parameter columns (batched models, element-major records
-     r = e * per + t): field fi with bit fi of fmask is stored once per
-     element (read at r / per); index column c with bit c of imask holds the
-     element's t = 0 position (column value = ix[r / per] + r % per).
-     Specialised modules only; 0 elsewhere. */
+  /* per-element parameter columns (batched models, element-major records):
+     element g of record r = r / per (kcol < 0) or ix[kcol][r] / per - g0,
+     instance k = r % per or ix[kcol][r] % per; field fi with bit fi of fmask
+     is stored per element (read at g); index column c with bit c of imask
+     holds the element's g(e) * per (column value = ix[c][g] + k).
+     Specialised modules only; 0 / -1 elsewhere. */
   int per;
   unsigned int fmask, imask;
+  int kcol;
+  int g0;
   int pad2;
 } ExaTerm;
 

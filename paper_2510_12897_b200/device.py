@@ -70,27 +70,73 @@ PERIODIC = os.environ.get("EXA_PERIODIC", "1") == "1"
 
 
 def _periodic(tp, period):
-    """(per, fmask, imask) of a term whose records are element-major over
-    ``period`` (r = e * period + t): field columns constant within every
-    element's run are stored once per element (fmask), index columns that
-    step by one within every run are stored as the run's first position
-    (imask).  MP models: branch admittances, costs, limits and the (bus,
-    period) variable positions; loads vary per period and stay per record.
-    (0, 0, 0) when nothing reduces."""
+    """Per-element parameter columns of a term of an element-major batched
+    model (records of element e over instances / periods k), or None.
+
+    The element of record r is ``r // period`` when every element has all
+    ``period`` records (``kcol = -1``: MP models, r = e * T + t), else
+    ``ix[kcol][r] // period - g0`` for an index column whose block position
+    ``h(e) * period + k`` names the element (N-1 flows: the flow variable of
+    a branch, whose instances skip the one with that branch out).  A field
+    column constant per element is stored once per element (bit ``fi`` of
+    fmask); an index column of the form ``g(e) * period + k`` (same instance
+    k as the record) is stored as ``g(e) * period`` per element (bit ``c`` of
+    imask).  Data-driven and exact: the stored tables reproduce every
+    record's value.  Returns dict(per, fmask, imask, kcol, g0, fcols,
+    icols) with the per-element tables, or None when nothing reduces."""
     n = tp.nrec
-    if not period or period < 2 or n == 0 or n % period:
-        return 0, 0, 0
-    fmask = imask = 0
-    for fi, nm in enumerate(tp.tape.field_names):
-        col = np.ascontiguousarray(tp.reals[nm], dtype=np.float64).view(np.int64).reshape(-1, period)
-        if np.all(col == col[:, :1]):
-            fmask |= 1 << fi
-    steps = np.arange(period, dtype=np.int64)[None, :]
-    for c, nm in enumerate(tp.tape.index_names):
-        col = np.asarray(tp.table.indices[nm], dtype=np.int64).reshape(-1, period) - steps
-        if np.all(col == col[:, :1]):
-            imask |= 1 << c
-    return (int(period) if (fmask or imask) else 0), fmask, imask
+    if not period or period < 2 or n == 0:
+        return None
+    P = int(period)
+    fields = [np.ascontiguousarray(tp.reals[nm], dtype=np.float64) for nm in tp.tape.field_names]
+    idx = [np.asarray(tp.table.indices[nm], dtype=np.int64) for nm in tp.tape.index_names]
+
+    def reduce_with(elem, first, kk, kcol):
+        """first[g] = a record of element g (elem = element of each record)."""
+        fmask = imask = 0
+        fcols, icols = {}, {}
+        for fi, col in enumerate(fields):
+            bits = col.view(np.int64)
+            tab = bits[first]
+            if np.all(bits == tab[elem]):
+                fmask |= 1 << fi
+                fcols[fi] = tab.view(np.float64)
+        for c, col in enumerate(idx):
+            if c == kcol:
+                continue
+            base = col - kk
+            tab = base[first]
+            if np.all(base == tab[elem]) and np.all(tab % P == 0):
+                imask |= 1 << c
+                icols[c] = tab
+        G = first.size  # per-element table length
+        saved = (8 * bin(fmask).count("1") + 4 * bin(imask).count("1")) * (n - G)
+        return saved, dict(per=P, fmask=fmask, imask=imask, kcol=kcol, fcols=fcols, icols=icols)
+
+    best = None
+    if n % P == 0:  # implicit element r // P
+        r = np.arange(n, dtype=np.int64)
+        cand = reduce_with(r // P, np.arange(0, n, P), r % P, -1)
+        cand[1]["g0"] = 0
+        if cand[0] > 0:
+            best = cand
+    for kc, key in enumerate(idx):  # element named by an index column
+        q = key // P
+        g0, g1 = int(q.min()), int(q.max())
+        if g1 - g0 + 1 > n:  # tables no larger than the columns they replace
+            continue
+        elem = q - g0
+        first = np.zeros(g1 - g0 + 1, dtype=np.int64)
+        first[elem[::-1]] = np.arange(n - 1, -1, -1)  # first record of each element
+        cand = reduce_with(elem, first, key % P, kc)
+        cand[1]["g0"] = g0
+        # a keyed load adds one dependent load: prefer the implicit form on ties
+        if cand[0] > 4 * n and (best is None or cand[0] > best[0] + 4 * n):
+            best = cand
+    if best is None or not (best[1]["fmask"] or best[1]["imask"]):
+        return None
+    return best[1]
+
 
 # Run heavy patterns in a separate concurrent kernel (measured slower on
 # case13659: the fork/join costs more than the register specialisation wins).
@@ -345,14 +391,14 @@ class HostLayout:
         self.scr0 = []
         period = getattr(plan, "batch_period", None) if (PERIODIC and self.specialised_ok) else None
         for t, tp in enumerate(terms):
-            per, fmask, imask = _periodic(tp, period)
+            red = _periodic(tp, period) or {"per": 0, "fmask": 0, "imask": 0, "kcol": -1, "g0": 0,
+                                            "fcols": {}, "icols": {}}
             d = {
-                "f_off": [f64.add(np.asarray(tp.reals[nm])[::per] if (fmask >> fi) & 1 else tp.reals[nm])
-                          for fi, nm in enumerate(tp.tape.field_names)],
-                "ix_off": [i32.add(_i32(np.asarray(tp.table.indices[nm])[::per] if (imask >> c) & 1
-                                        else tp.table.indices[nm], f"index column {nm!r}"))
+                "f_off": [f64.add(red["fcols"].get(fi, tp.reals[nm])) for fi, nm in enumerate(tp.tape.field_names)],
+                "ix_off": [i32.add(_i32(red["icols"].get(c, tp.table.indices[nm]), f"index column {nm!r}"))
                            for c, nm in enumerate(tp.tape.index_names)],
-                "per": per, "fmask": fmask, "imask": imask,
+                "per": red["per"], "fmask": red["fmask"], "imask": red["imask"], "kcol": red["kcol"],
+                "g0": red["g0"],
                 "voff": [blk.offset for blk in tp.slot_blocks],
                 "rows_off": i32.add(_i32(tp.rows, "augment rows")) if tp.kind == "augment" else -1,
                 "row_ptr_off": -1, "row_ent_off": -1,

@@ -350,7 +350,8 @@ def _specialised_kernels(layout, compressed: bool = False) -> str:
             lines.append(f"  T.{k} = {d[k]};")
         for k in ("jac0", "hess0", "scr0"):
             lines.append(f"  T.{k} = {d[k]}LL;")
-        lines.append(f"  T.per = {d.get('per', 0)}; T.fmask = {d.get('fmask', 0)}u; T.imask = {d.get('imask', 0)}u;")
+        lines.append(f"  T.per = {d.get('per', 0)}; T.fmask = {d.get('fmask', 0)}u; T.imask = {d.get('imask', 0)}u;"
+                     f" T.kcol = {d.get('kcol', -1)}; T.g0 = {d.get('g0', 0)};")
         lines.append("}")
         out.append("\n".join(lines))
     # per augment-target block: value of any contributing (term, record)

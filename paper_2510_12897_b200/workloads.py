@@ -85,10 +85,10 @@ def _term_param_bytes(tp, period) -> int:
     limits and (bus, period) variable positions)."""
     from .device import _periodic
 
-    per, fmask, imask = _periodic(tp, period)
+    red = _periodic(tp, period) or {"fcols": {}, "icols": {}}
     n = tp.nrec
-    b = sum(8 * (n // per if (fmask >> fi) & 1 else n) for fi in range(len(tp.tape.field_names)))
-    b += sum(4 * (n // per if (imask >> c) & 1 else n) for c in range(len(tp.tape.index_names)))
+    b = sum(8 * (red["fcols"][fi].size if fi in red["fcols"] else n) for fi in range(len(tp.tape.field_names)))
+    b += sum(4 * (red["icols"][c].size if c in red["icols"] else n) for c in range(len(tp.tape.index_names)))
     return b + (4 * n if tp.kind == "augment" else 0)
 
 
