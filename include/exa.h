@@ -218,22 +218,25 @@ int exa_pattern_create(ExaPlan* plan, int64_t n_raw, int64_t nnz, const int64_t*
  * plan whose kernels write those values. */
 int exa_pattern_create_known(ExaPlan* plan, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
                              const uint8_t* known, const double* known_val, ExaPattern** out);
-/* The Jacobian pattern for the compressed-set kernels (exa_plan_attach_compressed):
- * direct[r] != 0 flags raw slot r as written straight into its compressed
- * entry by the set kernel (0.0 + value, np.bincount's single-slot fold; the
- * entry must have exactly that one raw slot) -- those entries are left out
- * of the segmented sum.  Used by exa_eval_set_compressed only on a plan with
- * the compressed-set module attached. */
+/* A pattern for the compressed-set kernels (exa_plan_attach_compressed):
+ * direct[r] != 0 flags raw slot r as folded into its compressed entry by the
+ * set kernel itself (np.bincount's fold order); an entry whose slots other
+ * than known +0.0 are all direct is left out of the segmented sum, an entry
+ * mixing direct and other slots is an error.  Used by
+ * exa_eval_set_compressed only on a plan with the compressed-set module. */
 int exa_pattern_create_direct(ExaPlan* plan, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
                               const uint8_t* known, const double* known_val, const uint8_t* direct,
                               ExaPattern** out);
 void exa_pattern_destroy(ExaPattern* pattern);
 /* Attach the compressed-set module of a plan: a cubin (exa_jit_compile) with
  * set kernels exa_k_setc_h / exa_k_setc_l that write the direct compressed
- * Jacobian entries (ExaArgs.Jc) and keep every other raw slot in L2 for the
- * segmented sum.  Built host-side from the same layout as the plan's module
- * plus the direct entries' positions (paper_2510_12897_b200.device). */
-int exa_plan_attach_compressed(ExaPlan* plan, const void* cubin, int64_t cubin_size);
+ * Jacobian entries (ExaArgs.Jc) and the group-local compressed Hessian
+ * entries (ExaArgs.Hc, positions hpos[class * nrec + record], -1 = the
+ * record writes its raw slots instead) and keep every other raw slot in L2
+ * for the segmented sum.  Built host-side from the same layout as the
+ * plan's module (paper_2510_12897_b200.device); hpos is copied. */
+int exa_plan_attach_compressed(ExaPlan* plan, const void* cubin, int64_t cubin_size, const int32_t* hpos,
+                               int64_t n_hpos);
 /* cons + COMPRESSED Jacobian and Hessian values of one point: the set kernel
  * writes the raw slots into the workspace's scratch and the two segmented
  * sums run in one programmatic-dependent launch behind it (reference

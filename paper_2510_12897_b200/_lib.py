@@ -81,7 +81,7 @@ SIGNATURES = {
     "exa_pattern_create": (C.c_int, [vp, i64, i64, vp, vp, C.POINTER(vp)]),
     "exa_pattern_create_known": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, C.POINTER(vp)]),
     "exa_pattern_create_direct": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, C.POINTER(vp)]),
-    "exa_plan_attach_compressed": (C.c_int, [vp, vp, i64]),
+    "exa_plan_attach_compressed": (C.c_int, [vp, vp, i64, vp, i64]),
     "exa_pattern_destroy": (None, [vp]),
     "exa_eval_set_compressed": (C.c_int, [vp, vp, vp, vp, vp, vp, dbl, vp, vp, vp, vp]),
     "exa_eval_set_compressed_host": (C.c_int, [vp, vp, vp, vp, vp, vp, dbl, vp, vp, vp, vp]),

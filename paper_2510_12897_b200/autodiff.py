@@ -396,11 +396,15 @@ class CompressedPattern:
         runs, so the handle is shared by them."""
         handles = self.__dict__.setdefault("_exa_handles", {})
         # the plan's compressed-set kernels write the Jacobian entries of
-        # whole-row term blocks themselves (DevicePlan.jac_direct_mask, which
-        # also attaches those kernels to dp): such a pattern serves only plans
-        # with the same direct blocks
-        direct = dp.jac_direct_mask(self) if kind == "jac" else None
-        dsig = tuple(sorted(dp.layout.jdirect)) if direct is not None else None
+        # whole-row term blocks and the group-local Hessian entries themselves
+        # (DevicePlan.compressed_masks, which also attaches those kernels to
+        # dp): such a pattern serves only plans with the same direct entries
+        direct = dp.compressed_masks()[0 if kind == "jac" else 1] if kind in ("jac", "hess") else None
+        dsig = None
+        if direct is not None:
+            dsig = (tuple(sorted(dp.layout.jdirect)) if kind == "jac"
+                    else tuple(sorted((g, m, tuple(sorted(c))) for g, ms in dp.layout.hlocal.items()
+                                      for m, c in ms.items())))
         key = (dp.device, kind, bool(dp.exact_zero_sign) if kind else None, dsig)
         h = handles.get(key)
         if h is None:
@@ -420,7 +424,7 @@ class CompressedPattern:
                 for a, n, bits in runs:
                     known[a:a + n] = 1
                     val[a:a + n] = bits
-                if direct is not None:
+                if direct is not None:  # entries folded by the set kernel are left out
                     _lib.check(dp._lib.exa_pattern_create_direct(
                         dp.handle, int(self.slot_map.size), self.nnz, ptr.ctypes.data, ent.ctypes.data,
                         known.ctypes.data, val.ctypes.data, direct.ctypes.data, C.byref(h)),

@@ -820,11 +820,13 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
                 # column order -> entry jc0 + k r + rank of the slot's column;
                 # value 0.0 + v (np.bincount's single-slot fold)
                 rank = " + ".join(f"({cnames[m][t_]} < {cnames[m][s_]})" for t_ in range(k) if t_ != s_) or "0"
-                dst.append(f"  if (MODE & EXA_M_JAC) __stcs(A.Jc + ({int(jc0)}LL + {k}LL * r + ({rank})), "
-                           f"0.0 + {R(grads[s_])});")
+                # (no compressed Jacobian requested: the raw slot, as usual)
+                dst.append(f"  if (MODE & EXA_M_JAC) {{ if (A.Jc) __stcs(A.Jc + ({int(jc0)}LL + {k}LL * r + ({rank})), "
+                           f"0.0 + {R(grads[s_])}); else Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])}; }}")
                 continue
             dst.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
             dst.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
+        hcls = mem.get("hcls", {})  # compressed-set module: pair -> (class, position, class size)
         for seed in range(k):
             t = pc._tangents(g, v, seed)
             col = pc._slot_sums(g, pc._adjoint_tangents(g, v, adj, t))
@@ -836,7 +838,22 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
                     expr = f"({cnames[m][i]} == {cnames[m][j]} ? {expr} * 2.0 : {expr})"
                 pair = i * (i + 1) // 2 + j
                 if relax and _zero_const(col[i]):  # structural zero: +0.0, no weight
-                    early.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = 0.0;")
+                    # (compressed-set module with a compressed Hessian: the
+                    # segmented sum skips known +0.0 slots, nothing to write)
+                    guard = "(MODE & EXA_M_HESS) && !A.Hc" if mem.get("cmp") else "MODE & EXA_M_HESS"
+                    early.append(f"  if ({guard}) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = 0.0;")
+                    continue
+                if pair in hcls:
+                    # group-local compressed entry: its slots are this thread's
+                    # (one per member, members in raw-slot order): fold them in
+                    # np.bincount's order and store the entry; records where the
+                    # entry has other slots (hq < 0) write the raw slot instead
+                    c, q, size = hcls[pair]
+                    acc = "0.0 + hv_" if q == 0 else f"ha{c} + hv_"
+                    g.lines.append(f"  if (MODE & EXA_M_HESS) {{ const double hv_ = wgt{m} * {expr}; ha{c} = {acc}; "
+                                   f"if (hq{c} < 0) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = hv_; }}")
+                    if q == size - 1:
+                        g.lines.append(f"  if ((MODE & EXA_M_HESS) && hq{c} >= 0) __stcs(A.Hc + hq{c}, ha{c});")
                     continue
                 dst = early if (const(col[i]) and not dup) else g.lines
                 dst.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
@@ -862,6 +879,11 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
            "  double* __restrict__ Cout = A.c;", "  double* __restrict__ Jout = A.J;",
            "  double* __restrict__ Hout = A.H;", "  int rank = rank0;"]
     out.extend(pre)
+    # compressed-set module: positions of the group-local compressed H entries
+    # (plan data, loaded before the grid dependency) and their running folds
+    for c, off in sorted({c: off for _, mem in entries for (c, _q, _s, off) in mem.get("hcls_pos", [])}.items()):
+        out.append(f"  const int hq{c} = A.hpos ? __ldg(A.hpos + {int(off)}LL + r) : -1;  // -1: raw slots")
+        out.append(f"  double ha{c} = 0.0;")
     out.append(f"  EXA_TP(0, i{min(u_src)});" if u_src else "  EXA_TP(0, 0.0);")
     out.append("  EXA_GRID_WAIT();")
     out.extend(post)

@@ -142,6 +142,7 @@ struct ExaPlan {
      slots in L2 for the segmented sum */
   cudaLibrary_t lib_cmp = nullptr;
   cudaKernel_t kern_cmp[2] = {};
+  int32_t* hpos = nullptr; /* group-local compressed H entry per (class, record), -1 = not local */
   ExaWorkspace* dflt = nullptr;
   size_t bytes = 0;
   int pdl = 0;
@@ -849,6 +850,7 @@ void exa_plan_destroy(ExaPlan* p) {
   cudaFree(p->grad_ent);
   cudaFree(p->d2h);
   if (p->lib_cmp) cudaLibraryUnload(p->lib_cmp);
+  cudaFree(p->hpos);
   if (p->lib) cudaLibraryUnload(p->lib);
   delete p;
 }
@@ -1205,7 +1207,7 @@ struct DeviceGuard {
   if (int rc_ = reset_err(p, w, st)) return rc_;
 
 static int eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
-                    double* jac, double* hess, exa_stream_t stream, double* jac_c) {
+                    double* jac, double* hess, exa_stream_t stream, double* jac_c, double* hess_c) {
   EXA_PROLOGUE();
   A.x = x;
   A.y = mult;
@@ -1214,12 +1216,14 @@ static int eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double*
   A.J = jac;
   A.H = hess;
   A.Jc = jac_c;
-  return launch_mode(p, w, EXA_MODE_SET, A, st, 1, jac_c != nullptr);
+  A.Hc = hess_c;
+  A.hpos = hess_c ? p->hpos : nullptr;  // no compressed Hessian: raw slots everywhere
+  return launch_mode(p, w, EXA_MODE_SET, A, st, 1, jac_c != nullptr || hess_c != nullptr);
 }
 
 int exa_eval_set(ExaPlan* p, ExaWorkspace* ws, const double* x, const double* mult, double w_obj, double* c,
                  double* jac, double* hess, exa_stream_t stream) {
-  return eval_set(p, ws, x, mult, w_obj, c, jac, hess, stream, nullptr);
+  return eval_set(p, ws, x, mult, w_obj, c, jac, hess, stream, nullptr, nullptr);
 }
 
 int exa_eval_set_batch(ExaPlan* p, ExaWorkspace* ws, int64_t nsets, const double* x, const double* mult,
@@ -1587,16 +1591,18 @@ static int pattern_build(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* 
   std::vector<int32_t> order;
   order.reserve((size_t)nnz);
   for (int64_t k = 0; k < nnz; ++k) {
-    bool dir = false;
+    // an entry is left out when every slot that is not a known +0.0 is
+    // direct (folded by the set kernel); a partly direct entry is an error
+    int n_dir = 0, n_other = 0;
     if (direct)
-      for (int64_t e = ptr[k]; e < ptr[k + 1]; ++e)
-        if (direct[ent[e]]) {
-          if (ptr[k + 1] - ptr[k] != 1)
-            return fail("exa_pattern_create_direct: entry %lld has a direct slot among %lld slots", (long long)k,
-                        (long long)(ptr[k + 1] - ptr[k]));
-          dir = true;
-        }
-    if (!dir) order.push_back((int32_t)k);
+      for (int64_t e = ptr[k]; e < ptr[k + 1]; ++e) {
+        if (direct[ent[e]]) ++n_dir;
+        else if (cls(ent[e]) != 1) ++n_other;
+      }
+    if (n_dir && n_other)
+      return fail("exa_pattern_create_direct: entry %lld mixes %d direct with %d other slots", (long long)k, n_dir,
+                  n_other);
+    if (!n_dir) order.push_back((int32_t)k);
   }
   const int64_t n_fold = (int64_t)order.size();
   std::vector<int32_t> chk{0}, che{0}, chc{0}, src, eout((size_t)n_fold);
@@ -1705,10 +1711,17 @@ int exa_pattern_create_direct(ExaPlan* p, int64_t n_raw, int64_t nnz, const int6
   return pattern_build(p, n_raw, nnz, ptr, ent, known, known_val, out, direct);
 }
 
-int exa_plan_attach_compressed(ExaPlan* p, const void* cubin, int64_t cubin_size) {
-  if (!p || !cubin || cubin_size <= 0) return fail("exa_plan_attach_compressed: invalid argument");
+int exa_plan_attach_compressed(ExaPlan* p, const void* cubin, int64_t cubin_size, const int32_t* hpos,
+                               int64_t n_hpos) {
+  if (!p || !cubin || cubin_size <= 0 || n_hpos < 0 || (n_hpos && !hpos))
+    return fail("exa_plan_attach_compressed: invalid argument");
   if (p->lib_cmp) return 0;  // attached once per plan
   DeviceGuard g(p->device);
+  if (n_hpos) {
+    for (int64_t i = 0; i < n_hpos; ++i)
+      if (hpos[i] < -1) return fail("exa_plan_attach_compressed: bad entry position %d", hpos[i]);
+    if (int rc = dev_upload(&p->hpos, hpos, (size_t)n_hpos)) return rc;
+  }
   cudaLibrary_t lib = nullptr;
   cudaError_t e = cudaLibraryLoadData(&lib, cubin, nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e != cudaSuccess) return fail("cudaLibraryLoadData (compressed module): %s", cudaGetErrorString(e));
@@ -1756,12 +1769,16 @@ static int set_compressed(ExaPlan* p, ExaWorkspace* w, const ExaPattern* jp, con
   if (jp && hp && jp->ipt != hp->ipt) return fail("exa_eval_set_compressed: patterns chunked for different EXA_CMP_IPT");
   double* rawJ = jp ? w->dJ : jc;
   double* rawH = hp ? w->dH : hc;
-  if (jp && jp->direct && !(p->kern_cmp[0] && p->kern_cmp[1]))
-    return fail("exa_eval_set_compressed: direct Jacobian pattern but no compressed-set module attached");
-  if (hp && hp->direct) return fail("exa_eval_set_compressed: direct Hessian patterns are not supported");
+  if ((jp && jp->direct) || (hp && hp->direct)) {
+    if (!(p->kern_cmp[0] && p->kern_cmp[1]))
+      return fail("exa_eval_set_compressed: direct pattern but no compressed-set module attached");
+    if (hp && hp->direct && !p->hpos)
+      return fail("exa_eval_set_compressed: direct Hessian pattern but the plan has no entry positions");
+  }
   // direct J pattern: the compressed-set kernels write the direct entries into
   // jc themselves and every other raw slot into the workspace scratch
-  int rc = eval_set(p, w, x, mult, w_obj, c, rawJ, rawH, (exa_stream_t)st, jp && jp->direct ? jc : nullptr);
+  int rc = eval_set(p, w, x, mult, w_obj, c, rawJ, rawH, (exa_stream_t)st, jp && jp->direct ? jc : nullptr,
+                    hp && hp->direct ? hc : nullptr);
   if (rc) return rc;
   const int nchJ = jp ? jp->nch : 0, nchH = hp ? hp->nch : 0;
   if (nchJ + nchH == 0) return 0;

@@ -86,6 +86,8 @@ typedef struct ExaArgs {
   const int* i32;    /*   as blob + compile-time offsets)                    */
   long long* trace;  /* diagnostics timeline (EXA_TRACE modules), else 0 */
   double* Jc;        /* compressed Jacobian (compressed-set kernels: direct entries) */
+  double* Hc;        /* compressed Hessian (compressed-set kernels: group-local entries) */
+  const int* hpos;   /* ... their positions per (class, record), -1 = not local */
 } ExaArgs;
 
 /* domain-error key: order (20 bits) | instr (12 bits) | record+1 (32 bits) */

@@ -660,6 +660,79 @@ class HostLayout:
         self.jdirect = jdir
         return jdir, mask
 
+    def hess_local(self, hp):
+        """Group-local compressed Hessian entries: (hlocal, hpos, mask).
+
+        A *class* is a set of one H pair per term-group member (members in
+        raw-slot order) whose slots, for a record, are ALL the non-known
+        slots of one compressed entry of ``hp`` -- e.g. H(vm_f, va_t) of a
+        branch, to which exactly its four flow terms contribute.  The group
+        thread then folds the class in np.bincount's order (0.0 + the first
+        member's value + the next ...) and stores the entry itself.  Classes
+        are found on a sample of records (columns with equal entries) and
+        validated on every record; ``hpos[off + r]`` is the entry of record r,
+        or -1 where the entry has other slots too (parallel branches): that
+        record writes its raw slots for the segmented sum.  ``hlocal[gid][m]
+        = {pair: (class, position, size, off)}``; ``mask`` flags the raw H
+        slots folded in-thread (left out of the segmented sum)."""
+        known = np.zeros(hp.slot_map.size, dtype=bool)
+        for a, n_, _ in self.fill_hess:
+            known[a:a + n_] = True
+        cnt = np.bincount(hp.slot_map[~known], minlength=hp.nnz)
+        hlocal, pos, mask = {}, [], np.zeros(hp.slot_map.size, dtype=np.uint8)
+        at = ncls = 0
+        for gid, (_pid, grp, _members) in enumerate(self.groups):
+            cols = []  # (member, pair, raw slot of record 0)
+            n = self.terms[grp[0]].nrec
+            for m, u in enumerate(grp):
+                tp = self.terms[u]
+                if not tp.tape.k or tp.nrec != n:
+                    continue
+                for pr in tp.hess_pairs:
+                    if not known[pr.start]:
+                        cols.append((m, (pr.start - tp.hess_start) // n, pr.start))
+            if not cols or n == 0:
+                continue
+            E = np.stack([hp.slot_map[st:st + n] for _, _, st in cols])
+            samp = E[:, :: max(1, n // 4096)]
+            parent = list(range(len(cols)))
+
+            def find(a):
+                while parent[a] != a:
+                    parent[a] = parent[parent[a]]
+                    a = parent[a]
+                return a
+
+            for a in range(len(cols)):
+                for b in range(a + 1, len(cols)):
+                    if np.mean(samp[a] == samp[b]) > 0.5:
+                        parent[find(b)] = find(a)
+            classes: dict = {}
+            for a in range(len(cols)):
+                classes.setdefault(find(a), []).append(a)
+            for members in classes.values():
+                members.sort(key=lambda a: cols[a][2])  # raw-slot (fold) order
+                ms = [cols[a][0] for a in members]
+                if len(set(ms)) != len(ms) or ms != sorted(ms):
+                    continue  # one slot per member, members in fold order
+                e0 = E[members[0]]
+                valid = cnt[e0] == len(members)
+                for a in members[1:]:
+                    valid &= E[a] == e0
+                if valid.mean() < 0.5:
+                    continue
+                off = at
+                pos.append(np.where(valid, e0, -1).astype(np.int32))
+                at += n
+                for q, a in enumerate(members):
+                    m, pair, st = cols[a]
+                    hlocal.setdefault(gid, {}).setdefault(m, {})[pair] = (ncls, q, len(members), off)
+                    mask[st:st + n][valid] = 1
+                ncls += 1
+        self.hlocal = hlocal
+        hpos = np.concatenate(pos) if pos else np.zeros(0, dtype=np.int32)
+        return hlocal, hpos, mask
+
     def compressed_source(self) -> str:
         """CUDA source of the compressed-set module (set kernels
         ``exa_k_setc_h`` / ``_l``; needs :meth:`jac_direct` first)."""
@@ -1042,29 +1115,39 @@ class DevicePlan:
         self._ws_lock = threading.Lock()
         self._workspaces: list = []
 
-    def jac_direct_mask(self, jp):
-        """Raw Jacobian slots the compressed-set kernels write straight into
-        their compressed entries (``HostLayout.jac_direct``), after compiling
-        and attaching the plan's compressed-set module; None for generic
-        modules, no eligible term, or ``EXA_JDIRECT=0``."""
-        if hasattr(self, "_jdirect_mask"):
-            return self._jdirect_mask
-        self._jdirect_mask = None
+    def compressed_masks(self):
+        """(J mask, H mask): raw slots the compressed-set kernels fold into
+        their compressed entries themselves -- whole-row Jacobian blocks
+        (``HostLayout.jac_direct``) and group-local Hessian entries
+        (``HostLayout.hess_local``) -- after compiling and attaching the
+        plan's compressed-set module (once per plan); (None, None) for
+        generic modules, nothing eligible, or ``EXA_JDIRECT=0``."""
+        if hasattr(self, "_cmp_masks"):
+            return self._cmp_masks
+        self._cmp_masks = (None, None)
         lay = self.layout
         if not lay.specialised or os.environ.get("EXA_JDIRECT", "1") != "1":
-            return None
-        jdir, mask = lay.jac_direct(jp)
-        if not jdir:
-            return None
+            return self._cmp_masks
+        from .autodiff import model_patterns
+
+        jp, hp = model_patterns(self.model)
+        jdir, jmask = lay.jac_direct(jp)
+        hloc, hpos, hmask = lay.hess_local(hp) if os.environ.get("EXA_HLOCAL", "1") == "1" else ({}, None, None)
+        if not jdir and not hloc:
+            return self._cmp_masks
+        if not hloc:
+            lay.hlocal, hpos = {}, np.zeros(0, dtype=np.int32)
         cubin = compile_module(lay.compressed_source())
         buf = C.create_string_buffer(cubin, len(cubin))
+        hpos = np.ascontiguousarray(hpos, dtype=np.int32)
         import torch
 
         with torch.cuda.device(self.device):
-            _lib.check(self._lib.exa_plan_attach_compressed(self.handle, C.cast(buf, C.c_void_p), len(cubin)),
+            _lib.check(self._lib.exa_plan_attach_compressed(self.handle, C.cast(buf, C.c_void_p), len(cubin),
+                                                            hpos.ctypes.data if hpos.size else None, hpos.size),
                        "exa_plan_attach_compressed")
-        self._jdirect_mask = mask
-        return mask
+        self._cmp_masks = (jmask if jdir else None, hmask if hloc else None)
+        return self._cmp_masks
 
     def workspace(self) -> C.c_void_p:
         """The calling thread's workspace (objective / gradient scratch,

@@ -403,12 +403,25 @@ __device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, con
   if (WH) Hout[h0 + rec] = hv;
 }}""")
     jdir = getattr(layout, "jdirect", {}) if compressed else {}
+    hloc = getattr(layout, "hlocal", {}) if compressed else {}
+
+    def member_meta(gid, m, u, mem):
+        if not compressed:
+            return mem
+        extra = {"cmp": True}
+        if u in jdir:
+            extra["jc0"] = jdir[u]
+        cls = hloc.get(gid, {}).get(m)
+        if cls:
+            extra["hcls"] = {pair: (c, q, size) for pair, (c, q, size, _off) in cls.items()}
+            extra["hcls_pos"] = list(cls.values())
+        return dict(mem, **extra)
+
     for gid, (pid, grp, members) in enumerate(getattr(layout, "groups", [])):
         augs = [(layout.patterns[layout.term_pid[u]], off, m, s_)
                 for (u, off, m, s_) in getattr(layout, "group_augs", {}).get(gid, [])]
-        out.append(group_source(gid, [(layout.patterns[layout.term_pid[u]],
-                                       dict(mem, jc0=jdir[u]) if u in jdir else mem)
-                                      for u, mem in zip(grp, members)],
+        out.append(group_source(gid, [(layout.patterns[layout.term_pid[u]], member_meta(gid, m, u, mem))
+                                      for m, (u, mem) in enumerate(zip(grp, members))],
                                 augs, relax=layout.relax))
     if compressed:  # the compressed-set module: set kernels only
         for half, suffix in ((0, "_h"), (1, "_l")):

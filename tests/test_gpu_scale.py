@@ -227,3 +227,40 @@ def test_host_path_bitwise_at_scale(name, exact):
     for a, r in zip(p, ref):
         assert np.array_equal(a.view(np.int64), r)
     lib.exa_workspace_destroy(wsp)
+
+
+@pytest.mark.parametrize("name", ["case13659", "case1354"])
+def test_compressed_set_one_pattern_at_a_time(name):
+    """exa_eval_set_compressed with one pattern and the other output raw: the
+    compressed-set kernels fold only what is asked for (direct Jacobian
+    entries need jac_c, group-local Hessian entries hess_c) and write every
+    other raw slot -- bit for bit the plain set's raw slots / np.bincount."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2510_12897_b200 import _lib, model_patterns
+
+    model, (x, y, w) = workload(name)
+    c, J, H = _gpu_set(model, x, y, w)
+    jp, hp = model_patterns(model)
+    dp = model.device_plan
+    hj, hh = jp.device_handle(dp, "jac"), hp.device_handle(dp, "hess")
+    assert any(m is not None for m in dp.compressed_masks())
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    xd, yd = torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev)
+    st = torch.cuda.Stream(dev)
+    for jpat, hpat in ((hj, None), (None, hh), (hj, hh)):
+        cd = torch.full((model.ncon,), float("nan"), dtype=torch.float64, device=dev)
+        jd = torch.full((jp.nnz if jpat else model.plan.n_jac_slots,), float("nan"), dtype=torch.float64, device=dev)
+        hd = torch.full((hp.nnz if hpat else model.plan.n_hess_slots,), float("nan"), dtype=torch.float64, device=dev)
+        _lib.check(lib.exa_eval_set_compressed(dp.handle, None, jpat, hpat, xd.data_ptr(), yd.data_ptr(), w,
+                                               cd.data_ptr(), jd.data_ptr(), hd.data_ptr(),
+                                               C.c_void_p(st.cuda_stream)), "set_compressed")
+        st.synchronize()
+        wantJ = O.sum_values(jp.slot_map, jp.nnz, J) if jpat else J
+        wantH = O.sum_values(hp.slot_map, hp.nnz, H) if hpat else H
+        assert np.array_equal(cd.cpu().numpy().view(np.int64), c.view(np.int64))
+        assert np.array_equal(jd.cpu().numpy().view(np.int64), wantJ.view(np.int64))
+        assert np.array_equal(hd.cpu().numpy().view(np.int64), wantH.view(np.int64))

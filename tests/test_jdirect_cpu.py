@@ -72,3 +72,61 @@ def test_compressed_module_compiles():
     assert "exa_k_setc_l" in src and "exa_k_setc_h" in src and "A.Jc + (" in src
     cubin = compile_module(src)
     assert len(cubin) > 1000
+
+
+def _model_point(name):
+    if name.startswith("case13659"):
+        from paper_2510_12897_b200.workloads import build_workload, eval_inputs
+
+        model = build_workload("case13659", lower_to_gpu=False)
+        return model, eval_inputs(model, 0)
+    g = load(name)
+    return build(name, data=g), (g["x0"], g["y0"], float(g["w0"]))
+
+
+@pytest.mark.parametrize("name", ["syn30_mp6_polar", "case5_strg_mp4_polar", "case13659"])
+def test_group_local_hessian_classes(name):
+    """``HostLayout.hess_local``: for every valid (class, record) the class's
+    slots are exactly the compressed entry's slots other than known +0.0, in
+    raw-slot order, and folding the oracle's raw values in that order
+    (0.0 + v1 + v2 ...) is the oracle's sum_values bit for bit.  case13659
+    (groups of all four flows of a branch) has four-slot classes."""
+    model, (x, y, w) = _model_point(name)
+    plan = model.plan
+    lay = host_layout(plan)
+    hp = compress_coordinates(plan.hess_rows, plan.hess_cols)
+    hloc, hpos, mask = lay.hess_local(hp)
+    assert hloc
+    H = np.empty(plan.n_hess_slots)
+    O.eval_hessian(plan, x, y, w, H)
+    order_ = np.argsort(hp.slot_map, kind="stable")
+    ptr = np.zeros(hp.nnz + 1, dtype=np.int64)
+    np.cumsum(np.bincount(hp.slot_map, minlength=hp.nnz), out=ptr[1:])
+    Hc = O.sum_values(hp.slot_map, hp.nnz, H)
+    known = np.zeros(plan.n_hess_slots, dtype=bool)
+    for a, n, _ in lay.fill_hess:
+        known[a:a + n] = True
+    classes = {}
+    for gid, ms in hloc.items():
+        grp = lay.groups[gid][1]
+        for m, pairs in ms.items():
+            tp = lay.terms[grp[m]]
+            for pair, (c, q, size, off) in pairs.items():
+                classes.setdefault(c, {"off": off, "size": size, "slots": {}})["slots"][q] = (tp, pair)
+    if name == "case13659":
+        assert max(info["size"] for info in classes.values()) == 4
+    for c, info in classes.items():
+        order = [info["slots"][q] for q in range(info["size"])]
+        n = order[0][0].nrec
+        pos = hpos[info["off"]:info["off"] + n]
+        for r in np.flatnonzero(pos >= 0)[:200]:
+            raws = [tp.hess_start + pair * n + r for tp, pair in order]
+            assert raws == sorted(raws)
+            e = int(pos[r])
+            own = {int(t) for t in order_[ptr[e]:ptr[e + 1]] if not known[t]}
+            assert own == set(raws)
+            acc = 0.0
+            for s in raws:
+                acc = acc + H[s]
+            assert np.float64(acc).view(np.int64) == Hc[e].view(np.int64)
+            assert all(mask[s] for s in raws)

@@ -31,11 +31,8 @@ dev = torch.device("cuda", 0)
 t0 = time.time()
 plans = [DevicePlan(model, 0) for _ in range(R)]
 if os.environ.get("EXA_ATTACH_CMP") == "1":  # diagnostics: plans with the compressed-set module attached
-    from paper_2510_12897_b200 import model_patterns
-
-    _jp = model_patterns(model)[0]
     for _p in plans:
-        _p.jac_direct_mask(_jp)
+        _p.compressed_masks()
 tjit = time.time() - t0
 lib = _lib.load()
 bufs = []
