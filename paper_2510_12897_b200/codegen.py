@@ -839,16 +839,20 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
                 pair = i * (i + 1) // 2 + j
                 if relax and _zero_const(col[i]):  # structural zero: +0.0, no weight
                     # (compressed-set module with a compressed Hessian: the
-                    # segmented sum skips known +0.0 slots, nothing to write)
+                    # segmented sum skips known +0.0 slots, nothing to write;
+                    # an entry holding only this group's zeros is written here)
                     guard = "(MODE & EXA_M_HESS) && !A.Hc" if mem.get("cmp") else "MODE & EXA_M_HESS"
                     early.append(f"  if ({guard}) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = 0.0;")
+                    if pair in hcls and hcls[pair][1] == hcls[pair][2] - 1:
+                        c = hcls[pair][0]
+                        early.append(f"  if ((MODE & EXA_M_HESS) && hq{c} >= 0) __stcs(A.Hc + hq{c}, 0.0);")
                     continue
                 if pair in hcls:
                     # group-local compressed entry: its slots are this thread's
                     # (one per member, members in raw-slot order): fold them in
                     # np.bincount's order and store the entry; records where the
                     # entry has other slots (hq < 0) write the raw slot instead
-                    c, q, size = hcls[pair]
+                    c, q, size, _zero = hcls[pair]
                     acc = "0.0 + hv_" if q == 0 else f"ha{c} + hv_"
                     g.lines.append(f"  if (MODE & EXA_M_HESS) {{ const double hv_ = wgt{m} * {expr}; ha{c} = {acc}; "
                                    f"if (hq{c} < 0) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = hv_; }}")

@@ -679,59 +679,70 @@ class HostLayout:
         for a, n_, _ in self.fill_hess:
             known[a:a + n_] = True
         cnt = np.bincount(hp.slot_map[~known], minlength=hp.nnz)
+        cnt_all = np.bincount(hp.slot_map, minlength=hp.nnz)
         hlocal, pos, mask = {}, [], np.zeros(hp.slot_map.size, dtype=np.uint8)
         at = ncls = 0
         for gid, (_pid, grp, _members) in enumerate(self.groups):
-            cols = []  # (member, pair, raw slot of record 0)
             n = self.terms[grp[0]].nrec
-            for m, u in enumerate(grp):
-                tp = self.terms[u]
-                if not tp.tape.k or tp.nrec != n:
+            for zero in (False, True):
+                # value classes (slots that are not known +0.0), then classes of
+                # known +0.0 slots whose entries hold nothing else: the thread
+                # writes +0.0 there instead of the segmented sum
+                cols = []  # (member, pair, raw slot of record 0)
+                for m, u in enumerate(grp):
+                    tp = self.terms[u]
+                    if not tp.tape.k or tp.nrec != n:
+                        continue
+                    for pr in tp.hess_pairs:
+                        if bool(known[pr.start]) == zero:
+                            cols.append((m, (pr.start - tp.hess_start) // n, pr.start))
+                if not cols or n == 0:
                     continue
-                for pr in tp.hess_pairs:
-                    if not known[pr.start]:
-                        cols.append((m, (pr.start - tp.hess_start) // n, pr.start))
-            if not cols or n == 0:
-                continue
-            E = np.stack([hp.slot_map[st:st + n] for _, _, st in cols])
-            samp = E[:, :: max(1, n // 4096)]
-            parent = list(range(len(cols)))
-
-            def find(a):
-                while parent[a] != a:
-                    parent[a] = parent[parent[a]]
-                    a = parent[a]
-                return a
-
-            for a in range(len(cols)):
-                for b in range(a + 1, len(cols)):
-                    if np.mean(samp[a] == samp[b]) > 0.5:
-                        parent[find(b)] = find(a)
-            classes: dict = {}
-            for a in range(len(cols)):
-                classes.setdefault(find(a), []).append(a)
-            for members in classes.values():
-                members.sort(key=lambda a: cols[a][2])  # raw-slot (fold) order
-                ms = [cols[a][0] for a in members]
-                if len(set(ms)) != len(ms) or ms != sorted(ms):
-                    continue  # one slot per member, members in fold order
-                e0 = E[members[0]]
-                valid = cnt[e0] == len(members)
-                for a in members[1:]:
-                    valid &= E[a] == e0
-                if valid.mean() < 0.5:
-                    continue
-                off = at
-                pos.append(np.where(valid, e0, -1).astype(np.int32))
-                at += n
-                for q, a in enumerate(members):
-                    m, pair, st = cols[a]
-                    hlocal.setdefault(gid, {}).setdefault(m, {})[pair] = (ncls, q, len(members), off)
-                    mask[st:st + n][valid] = 1
-                ncls += 1
+                at, ncls = self._local_classes(hp, gid, n, cols, cnt_all if zero else cnt, zero, hlocal, pos,
+                                               mask, at, ncls)
         self.hlocal = hlocal
         hpos = np.concatenate(pos) if pos else np.zeros(0, dtype=np.int32)
         return hlocal, hpos, mask
+
+    def _local_classes(self, hp, gid, n, cols, cnt, zero, hlocal, pos, mask, at, ncls):
+        """Classes among ``cols`` of group ``gid`` (see :meth:`hess_local`)."""
+        E = np.stack([hp.slot_map[st:st + n] for _, _, st in cols])
+        samp = E[:, :: max(1, n // 4096)]
+        parent = list(range(len(cols)))
+
+        def find(a):
+            while parent[a] != a:
+                parent[a] = parent[parent[a]]
+                a = parent[a]
+            return a
+
+        for a in range(len(cols)):
+            for b in range(a + 1, len(cols)):
+                if np.mean(samp[a] == samp[b]) > 0.5:
+                    parent[find(b)] = find(a)
+        classes: dict = {}
+        for a in range(len(cols)):
+            classes.setdefault(find(a), []).append(a)
+        for members in classes.values():
+            members.sort(key=lambda a: cols[a][2])  # raw-slot (fold) order
+            ms = [cols[a][0] for a in members]
+            if len(set(ms)) != len(ms) or ms != sorted(ms):
+                continue  # one slot per member, members in fold order
+            e0 = E[members[0]]
+            valid = cnt[e0] == len(members)
+            for a in members[1:]:
+                valid &= E[a] == e0
+            if valid.mean() < 0.5:
+                continue
+            off = at
+            pos.append(np.where(valid, e0, -1).astype(np.int32))
+            at += n
+            for q, a in enumerate(members):
+                m, pair, st = cols[a]
+                hlocal.setdefault(gid, {}).setdefault(m, {})[pair] = (ncls, q, len(members), off, zero)
+                mask[st:st + n][valid] = 1
+            ncls += 1
+        return at, ncls
 
     def compressed_source(self) -> str:
         """CUDA source of the compressed-set module (set kernels

@@ -413,8 +413,8 @@ __device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, con
             extra["jc0"] = jdir[u]
         cls = hloc.get(gid, {}).get(m)
         if cls:
-            extra["hcls"] = {pair: (c, q, size) for pair, (c, q, size, _off) in cls.items()}
-            extra["hcls_pos"] = list(cls.values())
+            extra["hcls"] = {pair: (c, q, size, zero) for pair, (c, q, size, _off, zero) in cls.items()}
+            extra["hcls_pos"] = [(c, q, size, off) for (c, q, size, off, _zero) in cls.values()]
         return dict(mem, **extra)
 
     for gid, (pid, grp, members) in enumerate(getattr(layout, "groups", [])):

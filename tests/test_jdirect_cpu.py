@@ -111,8 +111,8 @@ def test_group_local_hessian_classes(name):
         grp = lay.groups[gid][1]
         for m, pairs in ms.items():
             tp = lay.terms[grp[m]]
-            for pair, (c, q, size, off) in pairs.items():
-                classes.setdefault(c, {"off": off, "size": size, "slots": {}})["slots"][q] = (tp, pair)
+            for pair, (c, q, size, off, zero) in pairs.items():
+                classes.setdefault(c, {"off": off, "size": size, "zero": zero, "slots": {}})["slots"][q] = (tp, pair)
     if name == "case13659":
         assert max(info["size"] for info in classes.values()) == 4
     for c, info in classes.items():
@@ -123,6 +123,10 @@ def test_group_local_hessian_classes(name):
             raws = [tp.hess_start + pair * n + r for tp, pair in order]
             assert raws == sorted(raws)
             e = int(pos[r])
+            if info["zero"]:  # the entry holds exactly these known +0.0 slots
+                assert {int(t) for t in order_[ptr[e]:ptr[e + 1]]} == set(raws) and all(known[s] for s in raws)
+                assert Hc[e] == 0.0 and not np.signbit(Hc[e])
+                continue
             own = {int(t) for t in order_[ptr[e]:ptr[e + 1]] if not known[t]}
             assert own == set(raws)
             acc = 0.0
