@@ -264,3 +264,41 @@ def test_compressed_set_one_pattern_at_a_time(name):
         assert np.array_equal(cd.cpu().numpy().view(np.int64), c.view(np.int64))
         assert np.array_equal(jd.cpu().numpy().view(np.int64), wantJ.view(np.int64))
         assert np.array_equal(hd.cpu().numpy().view(np.int64), wantH.view(np.int64))
+
+
+@pytest.mark.parametrize("name", ["case13659", "mp96_case1354"])
+def test_compressed_set_exact_zero_sign_at_scale(name):
+    """Compressed set on an exact zero-sign plan (structural Hessian zeros are
+    the reference's weight * 0.0, so they are folded like any slot and the
+    group-local classes include them): bit for bit np.bincount of the same
+    plan's raw slots, signs of zero included."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2510_12897_b200 import _lib, model_patterns
+    from paper_2510_12897_b200.device import DevicePlan
+
+    model, (x, y, w) = workload(name)
+    dp = DevicePlan(model, 0, exact_zero_sign=True)
+    jp, hp = model_patterns(model)
+    hj, hh = jp.device_handle(dp, "jac"), hp.device_handle(dp, "hess")
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    xd, yd = torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev)
+    st = torch.cuda.Stream(dev)
+    sh = C.c_void_p(st.cuda_stream)
+    n = (model.ncon, model.plan.n_jac_slots, model.plan.n_hess_slots)
+    raw = [torch.empty(k, dtype=torch.float64, device=dev) for k in n]
+    _lib.check(lib.exa_eval_set(dp.handle, None, xd.data_ptr(), yd.data_ptr(), w, *(t.data_ptr() for t in raw), sh),
+               "set")
+    cc = torch.empty(model.ncon, dtype=torch.float64, device=dev)
+    jc = torch.full((jp.nnz,), float("nan"), dtype=torch.float64, device=dev)
+    hc = torch.full((hp.nnz,), float("nan"), dtype=torch.float64, device=dev)
+    _lib.check(lib.exa_eval_set_compressed(dp.handle, None, hj, hh, xd.data_ptr(), yd.data_ptr(), w, cc.data_ptr(),
+                                           jc.data_ptr(), hc.data_ptr(), sh), "set_compressed")
+    st.synchronize()
+    J, H = raw[1].cpu().numpy(), raw[2].cpu().numpy()
+    assert np.array_equal(cc.cpu().numpy().view(np.int64), raw[0].cpu().numpy().view(np.int64))
+    assert np.array_equal(jc.cpu().numpy().view(np.int64), O.sum_values(jp.slot_map, jp.nnz, J).view(np.int64))
+    assert np.array_equal(hc.cpu().numpy().view(np.int64), O.sum_values(hp.slot_map, hp.nnz, H).view(np.int64))
