@@ -813,19 +813,39 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
         adj = pc._adjoints(g, v)
         grads = pc._slot_sums(g, adj)
         jc0 = mem.get("jc0")  # compressed-set module: this member's J entries are direct
+        jst = jc0 is not None and mem.get("jst")  # stage the warp's entries in shared memory
         for s_ in range(k):
-            dst = early if const(grads[s_]) else g.lines
-            if jc0 is not None:
-                # compressed J: the record's row holds exactly its k slots, in
-                # column order -> entry jc0 + k r + rank of the slot's column;
-                # value 0.0 + v (np.bincount's single-slot fold)
+            # (staged entries: after this member's flush of the previous one's)
+            dst = early if (const(grads[s_]) and not jst) else g.lines
+            if jc0 is not None and not jst:
                 rank = " + ".join(f"({cnames[m][t_]} < {cnames[m][s_]})" for t_ in range(k) if t_ != s_) or "0"
-                # (no compressed Jacobian requested: the raw slot, as usual)
                 dst.append(f"  if (MODE & EXA_M_JAC) {{ if (A.Jc) __stcs(A.Jc + ({int(jc0)}LL + {k}LL * r + ({rank})), "
                            f"0.0 + {R(grads[s_])}); else Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])}; }}")
                 continue
+            if jc0 is not None:
+                # compressed J: the record's row holds exactly its k slots, in
+                # column order -> entry jc0 + k r + rank of the slot's column;
+                # value 0.0 + v (np.bincount's single-slot fold).  The warp's
+                # 32 consecutive records own k * 32 consecutive entries: staged
+                # in shared memory (EXA_JST) and stored coalesced below.
+                rank = " + ".join(f"({cnames[m][t_]} < {cnames[m][s_]})" for t_ in range(k) if t_ != s_) or "0"
+                # (no compressed Jacobian requested: the raw slot, as usual)
+                dst.append(f"  if (MODE & EXA_M_JAC) {{ if (A.Jc) EXA_JST[(threadIdx.x & 31) * {k} + ({rank})] = "
+                           f"0.0 + {R(grads[s_])}; else Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])}; }}")
+                continue
             dst.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
             dst.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
+        if jst and k:
+            # the warp's lanes hold consecutive records r0 .. r0 + nact - 1
+            # (lanes past the block's last record have returned)
+            # (the mask comes from the record count, not __activemask(): every
+            # lane of it must reach the barrier, converged or not)
+            g.lines.append(f"  if ((MODE & EXA_M_JAC) && A.Jc) {{ const int lane_ = threadIdx.x & 31, r0_ = r - lane_; "
+                           f"const int nact_ = min(32, {T}.nrec - r0_); "
+                           f"const unsigned act_ = nact_ >= 32 ? 0xffffffffu : ((1u << nact_) - 1u); __syncwarp(act_); "
+                           f"double* __restrict__ jd_ = A.Jc + {int(jc0)}LL + {k}LL * r0_; "
+                           f"for (int i_ = lane_; i_ < {k} * nact_; i_ += 32) __stcs(jd_ + i_, EXA_JST[i_]); "
+                           f"__syncwarp(act_); }}")
         hcls = mem.get("hcls", {})  # compressed-set module: pair -> (class, position, class size)
         for seed in range(k):
             t = pc._tangents(g, v, seed)
@@ -883,6 +903,10 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
            "  double* __restrict__ Cout = A.c;", "  double* __restrict__ Jout = A.J;",
            "  double* __restrict__ Hout = A.H;", "  int rank = rank0;"]
     out.extend(pre)
+    kst = max((pc.k for pc, mem in entries if mem.get("jc0") is not None and mem.get("jst")), default=0)
+    if kst:  # this warp's stage of direct Jacobian entries (32 records x k slots)
+        out.append(f"  __shared__ double exa_jst_[EXA_JST_WARPS * 32 * {kst}];")
+        out.append(f"  double* const EXA_JST = exa_jst_ + (threadIdx.x >> 5) * 32 * {kst};")
     # compressed-set module: positions of the group-local compressed H entries
     # (plan data, loaded before the grid dependency) and their running folds
     for c, off in sorted({c: off for _, mem in entries for (c, _q, _s, off) in mem.get("hcls_pos", [])}.items()):

@@ -684,7 +684,7 @@ class HostLayout:
         at = ncls = 0
         for gid, (_pid, grp, _members) in enumerate(self.groups):
             n = self.terms[grp[0]].nrec
-            for zero in (False, True):
+            for zero in ((False, True) if os.environ.get("EXA_HLOCAL_ZERO", "1") == "1" else (False,)):
                 # value classes (slots that are not known +0.0), then classes of
                 # known +0.0 slots whose entries hold nothing else: the thread
                 # writes +0.0 there instead of the segmented sum

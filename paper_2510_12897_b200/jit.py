@@ -411,6 +411,12 @@ __device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, con
         extra = {"cmp": True}
         if u in jdir:
             extra["jc0"] = jdir[u]
+            # many-wave sets (256-thread CTAs): stage the warp's direct entries
+            # in shared memory and store them coalesced (MP96 compressed set
+            # 111 -> 99 us); one-wave sets store them where they are computed
+            # (case13659 14.3 vs 15.8 us staged: the extra barriers sit on the
+            # critical path)
+            extra["jst"] = layout.threads[1] > 32
         cls = hloc.get(gid, {}).get(m)
         if cls:
             extra["hcls"] = {pair: (c, q, size, zero) for pair, (c, q, size, _off, zero) in cls.items()}
@@ -736,6 +742,8 @@ def module_source(patterns, layout=None, threads: int = 32, compressed: bool = F
     else:
         parts.append(_specialised_kernels(layout, compressed))
     bl = f"{threads}, {min_blocks(threads)}"
+    # warps per CTA of the largest kernel (per-warp shared stages, EXA_JST)
+    parts.insert(1, f"#define EXA_JST_WARPS {max(threads, THREADS_HEAVY) // 32}")
     return "\n".join(parts).replace("@BOUNDS_L@", bl).replace("@BOUNDS_H@", str(THREADS_HEAVY))
 
 
