@@ -743,7 +743,7 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
     va_t) -- is computed once (the generator's CSE), while each member's
     outputs keep the reference's per-term operation order.
 
-    ``augs[k] = (PatternCode, record offset, member, slot)``: in the set kernel
+    ``augs[k] = (PatternCode, record offset, member, slot[, row source])``: in the set kernel
     the group also writes the J/H slots of augment ``U<k>``'s records
     ``off + r`` (single-variable, field-free pattern gathering the same
     variable as the member's slot), weighted by the multiplier of the row the
@@ -883,13 +883,17 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
                 dst.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
     # attached augments: their J slots in the jac/set kernels, H in hess/set
     aug_late = []
-    for k, (apc, off, m, s_) in enumerate(augs):
+    for k, aug in enumerate(augs):
+        apc, off, m, s_ = aug[:4]
+        rowsrc = aug[4] if len(aug) > 4 else None
         xs = vsyms[m][s_].name
         if relax and getattr(apc, "termx_hzero", False):
             # structural-zero Hessian entry: written as +0.0 (the reference's
             # w * 0.0 carries the multiplier's sign; IEEE-equal, see the zero-sign
             # relaxation) -- saves a two-load chain per record
             post.append(f"  const double wa{k} = 0.0;")
+        elif rowsrc is not None:  # row = constant + a group index column: one load
+            post.append(f"  const double wa{k} = !(MODE & EXA_M_HESS) ? 0.0 : __ldg(A.y + ({rowsrc[1]}LL + i{rowsrc[0]}));")
         else:
             post.append(f"  const double wa{k} = !(MODE & EXA_M_HESS) ? 0.0 : __ldg(A.y + __ldg(U{k}.rows + {off} + r));")
         dst = early if getattr(apc, "termx_const", False) else aug_late

@@ -20,6 +20,8 @@ import re
 import threading
 from pathlib import Path
 
+import numpy as np
+
 from . import _lib
 from .codegen import group_source
 
@@ -424,7 +426,7 @@ __device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, con
         return dict(mem, **extra)
 
     for gid, (pid, grp, members) in enumerate(getattr(layout, "groups", [])):
-        augs = [(layout.patterns[layout.term_pid[u]], off, m, s_)
+        augs = [(layout.patterns[layout.term_pid[u]], off, m, s_, _aug_row_source(layout, grp, members, u, off))
                 for (u, off, m, s_) in getattr(layout, "group_augs", {}).get(gid, [])]
         out.append(group_source(gid, [(layout.patterns[layout.term_pid[u]], member_meta(gid, m, u, mem))
                                       for m, (u, mem) in enumerate(zip(grp, members))],
@@ -437,6 +439,28 @@ __device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, con
             for half, suffix in ((0, "_h"), (1, "_l")):
                 out.append(_kernel_source(layout, m, half, name + suffix))
     return _cache_hints("\n\n".join(out))
+
+
+def _aug_row_source(layout, grp, members, u, off):
+    """(group index column id, constant) when an attached augment's rows are
+    ``constant + that index column`` record for record (OPF: the balance row
+    of the bus a flow's from-/to-end index names, ``row_offset + i``): the
+    group then loads the row's multiplier directly, without the augment's
+    row column in between (exact zero-sign mode: its w * 0 Hessian entry).
+    None otherwise."""
+    a = layout.terms[u]
+    n = layout.terms[grp[0]].nrec
+    rows = np.asarray(a.rows, dtype=np.int64)[off:off + n]
+    for m, t in enumerate(grp):
+        tp = layout.terms[t]
+        for c, nm in enumerate(tp.tape.index_names):
+            col = np.asarray(tp.table.indices[nm], dtype=np.int64)
+            if col.size != n:
+                continue
+            d = rows - col
+            if d.size and np.all(d == d[0]):
+                return members[m]["cols"][c], int(d[0])
+    return None
 
 
 def _cache_hints(src: str) -> str:
