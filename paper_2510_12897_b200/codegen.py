@@ -839,12 +839,14 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
             # the warp's lanes hold consecutive records r0 .. r0 + nact - 1
             # (lanes past the block's last record have returned)
             # (the mask comes from the record count, not __activemask(): every
-            # lane of it must reach the barrier, converged or not)
+            # lane of it must reach the barrier, converged or not; the store
+            # loop strides by the live lanes -- in the block's last, partial
+            # warp the lanes past its last record have returned)
             g.lines.append(f"  if ((MODE & EXA_M_JAC) && A.Jc) {{ const int lane_ = threadIdx.x & 31, r0_ = r - lane_; "
                            f"const int nact_ = min(32, {T}.nrec - r0_); "
                            f"const unsigned act_ = nact_ >= 32 ? 0xffffffffu : ((1u << nact_) - 1u); __syncwarp(act_); "
                            f"double* __restrict__ jd_ = A.Jc + {int(jc0)}LL + {k}LL * r0_; "
-                           f"for (int i_ = lane_; i_ < {k} * nact_; i_ += 32) __stcs(jd_ + i_, EXA_JST[i_]); "
+                           f"for (int i_ = lane_; i_ < {k} * nact_; i_ += nact_) __stcs(jd_ + i_, EXA_JST[i_]); "
                            f"__syncwarp(act_); }}")
         hcls = mem.get("hcls", {})  # compressed-set module: pair -> (class, position, class size)
         for seed in range(k):

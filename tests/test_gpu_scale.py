@@ -302,3 +302,24 @@ def test_compressed_set_exact_zero_sign_at_scale(name):
     assert np.array_equal(cc.cpu().numpy().view(np.int64), raw[0].cpu().numpy().view(np.int64))
     assert np.array_equal(jc.cpu().numpy().view(np.int64), O.sum_values(jp.slot_map, jp.nnz, J).view(np.int64))
     assert np.array_equal(hc.cpu().numpy().view(np.int64), O.sum_values(hp.slot_map, hp.nnz, H).view(np.int64))
+
+
+def test_compressed_set_n1_batch():
+    """Compressed set on an N-1 batch (64 contingencies of the case2000-shaped
+    network: keyed per-element parameter columns, many-wave compressed-set
+    kernels with staged Jacobian entries): bit for bit np.bincount of the
+    plan's raw slots."""
+    from paper_2510_12897_b200 import eval_callback_set_compressed, model_patterns
+    from paper_2510_12897_b200.scopf import scopf_model
+    from paper_2510_12897_b200.synth import evaluation_point, pglib_shaped
+
+    model = scopf_model(pglib_shaped("case2000", seed=1), list(range(64)), lower_to_gpu=True)[0]
+    assert any(d.get("per") for d in model.device_plan.layout.descs)
+    x, y, w = evaluation_point(model, 3)
+    c, J, H = _gpu_set(model, x, y, w)
+    jp, hp = model_patterns(model)
+    cc, Jc, Hc = np.empty(model.ncon), np.empty(jp.nnz), np.empty(hp.nnz)
+    eval_callback_set_compressed(model, x, y, w, cc, Jc, Hc)
+    assert np.array_equal(cc.view(np.int64), c.view(np.int64))
+    assert np.array_equal(Jc.view(np.int64), O.sum_values(jp.slot_map, jp.nnz, J).view(np.int64))
+    assert np.array_equal(Hc.view(np.int64), O.sum_values(hp.slot_map, hp.nnz, H).view(np.int64))
