@@ -812,36 +812,34 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
         g.deriv = relax
         adj = pc._adjoints(g, v)
         grads = pc._slot_sums(g, adj)
-        jc0 = mem.get("jc0")  # compressed-set module: this member's J entries are direct
-        jst = jc0 is not None and mem.get("jst")  # stage the warp's entries in shared memory
+        # compressed-set module, direct member: the record's Jacobian row holds
+        # exactly its k slots, in column order -> slot s is entry jc0 + k r +
+        # rank (how many of the record's other columns are smaller), value
+        # 0.0 + v (np.bincount's single-slot fold); without a compressed
+        # Jacobian (A.Jc null) the raw slot as usual.  jst: the warp's 32
+        # consecutive records own k * 32 consecutive entries -- staged in
+        # shared memory (EXA_JST) and stored coalesced after the last slot.
+        jc0 = mem.get("jc0")
+        jst = jc0 is not None and mem.get("jst")
         for s_ in range(k):
-            # (staged entries: after this member's flush of the previous one's)
+            # (staged entries go after the previous member's flush: no early)
             dst = early if (const(grads[s_]) and not jst) else g.lines
-            if jc0 is not None and not jst:
-                rank = " + ".join(f"({cnames[m][t_]} < {cnames[m][s_]})" for t_ in range(k) if t_ != s_) or "0"
-                dst.append(f"  if (MODE & EXA_M_JAC) {{ if (A.Jc) __stcs(A.Jc + ({int(jc0)}LL + {k}LL * r + ({rank})), "
-                           f"0.0 + {R(grads[s_])}); else Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])}; }}")
-                continue
             if jc0 is not None:
-                # compressed J: the record's row holds exactly its k slots, in
-                # column order -> entry jc0 + k r + rank of the slot's column;
-                # value 0.0 + v (np.bincount's single-slot fold).  The warp's
-                # 32 consecutive records own k * 32 consecutive entries: staged
-                # in shared memory (EXA_JST) and stored coalesced below.
                 rank = " + ".join(f"({cnames[m][t_]} < {cnames[m][s_]})" for t_ in range(k) if t_ != s_) or "0"
-                # (no compressed Jacobian requested: the raw slot, as usual)
-                dst.append(f"  if (MODE & EXA_M_JAC) {{ if (A.Jc) EXA_JST[(threadIdx.x & 31) * {k} + ({rank})] = "
-                           f"0.0 + {R(grads[s_])}; else Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])}; }}")
+                tgt = (f"EXA_JST[(threadIdx.x & 31) * {k} + ({rank})] =" if jst
+                       else f"__stcs(A.Jc + ({int(jc0)}LL + {k}LL * r + ({rank})),")
+                close = ";" if jst else ");"
+                dst.append(f"  if (MODE & EXA_M_JAC) {{ if (A.Jc) {tgt} 0.0 + {R(grads[s_])}{close} "
+                           f"else Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])}; }}")
                 continue
             dst.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
             dst.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
         if jst and k:
-            # the warp's lanes hold consecutive records r0 .. r0 + nact - 1
-            # (lanes past the block's last record have returned)
-            # (the mask comes from the record count, not __activemask(): every
-            # lane of it must reach the barrier, converged or not; the store
-            # loop strides by the live lanes -- in the block's last, partial
-            # warp the lanes past its last record have returned)
+            # the warp's lanes hold consecutive records r0 .. r0 + nact - 1; in
+            # the block's last, partial warp the lanes past its last record
+            # have returned, so the mask comes from the record count (not
+            # __activemask(): every lane of it must reach the barrier,
+            # converged or not) and the store loop strides by the live lanes
             g.lines.append(f"  if ((MODE & EXA_M_JAC) && A.Jc) {{ const int lane_ = threadIdx.x & 31, r0_ = r - lane_; "
                            f"const int nact_ = min(32, {T}.nrec - r0_); "
                            f"const unsigned act_ = nact_ >= 32 ? 0xffffffffu : ((1u << nact_) - 1u); __syncwarp(act_); "
