@@ -731,6 +731,24 @@ class PatternCode:
         return list(self.tape.instr)
 
 
+def _jst_flush(members, tail_sync: bool) -> str:
+    """Coalesced stores of staged direct-Jacobian entries.  The warp's lanes
+    hold consecutive records r0 .. r0 + nact - 1; in the block's last,
+    partial warp the lanes past its last record have returned, so the mask
+    comes from the record count (not __activemask(): every lane of it must
+    reach the barrier, converged or not) and the store loops stride by the
+    live lanes.  ``tail_sync``: the stage is reused after the flush."""
+    T0 = members[0][3]
+    fl = [f"  if ((MODE & EXA_M_JAC) && A.Jc) {{ const int lane_ = threadIdx.x & 31, r0_ = r - lane_; "
+          f"const int nact_ = min(32, {T0}.nrec - r0_); "
+          f"const unsigned act_ = nact_ >= 32 ? 0xffffffffu : ((1u << nact_) - 1u); __syncwarp(act_);"]
+    for (_m, k_, jc0_, _T, off_) in members:
+        fl.append(f" {{ double* __restrict__ jd_ = A.Jc + {jc0_}LL + {k_}LL * r0_; "
+                  f"for (int i_ = lane_; i_ < {k_} * nact_; i_ += nact_) __stcs(jd_ + i_, EXA_JST[{off_} + i_]); }}")
+    fl.append(" __syncwarp(act_); }" if tail_sync else " }")
+    return "".join(fl)
+
+
 def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = None) -> str:
     """One thread evaluates record r of several terms (a *term group*).
 
@@ -798,6 +816,8 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
     def const(v) -> bool:
         return not isinstance(v, Sym)
 
+    # staged direct-Jacobian members still to flush: (m, k, jc0, T, stage offset)
+    jst_members, jst_off, jst_size = [], 0, 0
     for m, (pc, mem) in enumerate(entries):
         k = pc.k
         T = f"T{m}"
@@ -820,13 +840,17 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
         # consecutive records own k * 32 consecutive entries -- staged in
         # shared memory (EXA_JST) and stored coalesced after the last slot.
         jc0 = mem.get("jc0")
-        jst = jc0 is not None and mem.get("jst")
+        jst = mem.get("jst") if jc0 is not None else None  # "member" / "group" flush, or None
+        if jst == "member":  # the member's own stage, flushed after its last slot
+            jst_off = 0
+        if jst:
+            jst_members.append((m, k, int(jc0), T, jst_off))
         for s_ in range(k):
-            # (staged entries go after the previous member's flush: no early)
-            dst = early if (const(grads[s_]) and not jst) else g.lines
+            # ("member" stages share one buffer: after the previous member's flush)
+            dst = early if (const(grads[s_]) and jst != "member") else g.lines
             if jc0 is not None:
                 rank = " + ".join(f"({cnames[m][t_]} < {cnames[m][s_]})" for t_ in range(k) if t_ != s_) or "0"
-                tgt = (f"EXA_JST[(threadIdx.x & 31) * {k} + ({rank})] =" if jst
+                tgt = (f"EXA_JST[{jst_off} + (threadIdx.x & 31) * {k} + ({rank})] =" if jst
                        else f"__stcs(A.Jc + ({int(jc0)}LL + {k}LL * r + ({rank})),")
                 close = ";" if jst else ");"
                 dst.append(f"  if (MODE & EXA_M_JAC) {{ if (A.Jc) {tgt} 0.0 + {R(grads[s_])}{close} "
@@ -834,18 +858,12 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
                 continue
             dst.append(f"  if ((MODE & EXA_M_JAC) && {T}.kind != EXA_OBJ) Jout[{T}.jac0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
             dst.append(f"  if ((MODE & EXA_M_GRAD) && {T}.kind == EXA_OBJ) A.G[{T}.scr0 + {s_}LL * {T}.nrec + r] = {R(grads[s_])};")
-        if jst and k:
-            # the warp's lanes hold consecutive records r0 .. r0 + nact - 1; in
-            # the block's last, partial warp the lanes past its last record
-            # have returned, so the mask comes from the record count (not
-            # __activemask(): every lane of it must reach the barrier,
-            # converged or not) and the store loop strides by the live lanes
-            g.lines.append(f"  if ((MODE & EXA_M_JAC) && A.Jc) {{ const int lane_ = threadIdx.x & 31, r0_ = r - lane_; "
-                           f"const int nact_ = min(32, {T}.nrec - r0_); "
-                           f"const unsigned act_ = nact_ >= 32 ? 0xffffffffu : ((1u << nact_) - 1u); __syncwarp(act_); "
-                           f"double* __restrict__ jd_ = A.Jc + {int(jc0)}LL + {k}LL * r0_; "
-                           f"for (int i_ = lane_; i_ < {k} * nact_; i_ += nact_) __stcs(jd_ + i_, EXA_JST[i_]); "
-                           f"__syncwarp(act_); }}")
+        if jst:
+            jst_off += 32 * k
+            jst_size = max(jst_size, jst_off)
+        if jst == "member":
+            g.lines.append(_jst_flush(jst_members[-1:], tail_sync=True))
+            jst_members.clear()
         hcls = mem.get("hcls", {})  # compressed-set module: pair -> (class, position, class size)
         for seed in range(k):
             t = pc._tangents(g, v, seed)
@@ -881,6 +899,8 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
                     continue
                 dst = early if (const(col[i]) and not dup) else g.lines
                 dst.append(f"  if (MODE & EXA_M_HESS) Hout[{T}.hess0 + {pair}LL * {T}.nrec + r] = wgt{m} * {expr};")
+    if jst_members:  # "group": one flush of every member's entries after the group's work
+        g.lines.append(_jst_flush(jst_members, tail_sync=False))
     # attached augments: their J slots in the jac/set kernels, H in hess/set
     aug_late = []
     for k, aug in enumerate(augs):
@@ -907,10 +927,9 @@ def group_source(gid: int, entries: list, augs: list = (), relax: bool | None = 
            "  double* __restrict__ Cout = A.c;", "  double* __restrict__ Jout = A.J;",
            "  double* __restrict__ Hout = A.H;", "  int rank = rank0;"]
     out.extend(pre)
-    kst = max((pc.k for pc, mem in entries if mem.get("jc0") is not None and mem.get("jst")), default=0)
-    if kst:  # this warp's stage of direct Jacobian entries (32 records x k slots)
-        out.append(f"  __shared__ double exa_jst_[EXA_JST_WARPS * 32 * {kst}];")
-        out.append(f"  double* const EXA_JST = exa_jst_ + (threadIdx.x >> 5) * 32 * {kst};")
+    if jst_size:  # this warp's stage of direct Jacobian entries (32 records x k slots per member)
+        out.append(f"  __shared__ double exa_jst_[EXA_JST_WARPS * {jst_size}];")
+        out.append(f"  double* const EXA_JST = exa_jst_ + (threadIdx.x >> 5) * {jst_size};")
     # compressed-set module: positions of the group-local compressed H entries
     # (plan data, loaded before the grid dependency) and their running folds
     for c, off in sorted({c: off for _, mem in entries for (c, _q, _s, off) in mem.get("hcls_pos", [])}.items()):

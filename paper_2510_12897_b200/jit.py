@@ -418,7 +418,8 @@ __device__ __forceinline__ void exa_bkout_T{t}(const int e, const double xv, con
             # 111 -> 99 us); one-wave sets store them where they are computed
             # (case13659 14.3 vs 15.8 us staged: the extra barriers sit on the
             # critical path)
-            extra["jst"] = layout.threads[1] > 32
+            extra["jst"] = ("member" if layout.threads[1] > 32
+                            else ("group" if os.environ.get("EXA_JST_ONEWAVE") == "1" else None))
         cls = hloc.get(gid, {}).get(m)
         if cls:
             extra["hcls"] = {pair: (c, q, size, zero) for pair, (c, q, size, _off, zero) in cls.items()}
