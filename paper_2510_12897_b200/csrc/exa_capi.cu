@@ -1101,7 +1101,9 @@ int exa_plan_create(const ExaPlanDesc* d, ExaPlan** out) {
       p->grid[kid] = need < occ * n_sm ? need : occ * n_sm;
     }
   }
-  if (cudaLibraryGetKernel(&p->kern_batch, p->lib, "exa_k_setb_l") != cudaSuccess) {
+  // the strided-batch entry exists in model-specialised modules only (the
+  // descriptor says so): no failing symbol lookup for generic modules
+  if (d->batchable && cudaLibraryGetKernel(&p->kern_batch, p->lib, "exa_k_setb_l") != cudaSuccess) {
     cudaGetLastError();
     p->kern_batch = nullptr;
   }
