@@ -357,6 +357,55 @@ def graph_us(launch, n, stream, dev, reps=5):
     return e0.elapsed_time(e1) * 1e3 / (reps * n)
 
 
+def streams_leg(lib, plans, bufs, stream, dev, bps, peak, n_streams=2, reps=5):
+    """Extra, not the headline: the same independent sets, one fused launch
+    each, spread over ``n_streams`` concurrent streams (replica r always on
+    stream r % n_streams, so each plan's workspace serves one stream), as
+    several solver instances evaluating side by side would run.  One graph:
+    the side streams fork from and join the launching stream, on which the
+    CUDA events time it."""
+    import torch
+
+    R = len(plans)
+    sts = [stream] + [torch.cuda.Stream(dev) for _ in range(n_streams - 1)]
+    ls = [launcher(lib, plans, bufs, s) for s in sts]
+
+    def launch(i):
+        ls[(i % R) % n_streams](i)
+
+    n = R * max(1, 512 // R)
+    for i in range(R):
+        launch(i)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        for s in sts[1:]:
+            s.wait_event(fork)
+        for i in range(n):
+            launch(i)
+        for s in sts[1:]:
+            join = torch.cuda.Event()
+            join.record(s)
+            stream.wait_event(join)
+    with torch.cuda.stream(stream):
+        g.replay()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    us = e0.elapsed_time(e1) * 1e3 / (reps * n)
+    return {"n_streams": n_streams, "us_per_set": us, "value": 1e6 / us, "unit": "sets/s",
+            "roofline_frac": bps / us / 1e3 / peak,
+            "note": "extra, not the headline: independent sets, one launch each, on concurrent streams "
+                    "(several solver instances side by side); the headline is one stream"}
+
+
 def isolated_latency_us(launch, stream, dev, n=40):
     """One set with nothing before or after it on the stream (an IPM evaluates
     one set per iteration): median of per-launch CUDA-event intervals."""
@@ -689,6 +738,8 @@ def main():
         extras["callbacks"] = cb
         # ---- compressed J/H (the values the reference solver consumes)
         extras["compressed"] = compressed_leg(model, plans, bufs, lib, stream, dev, peak)
+        # ---- the same sets on two concurrent streams
+        extras["streams"] = streams_leg(lib, plans, bufs, stream, dev, bps, peak)
 
     # ---- extra (not the headline): NB independent sets per launch
     # (exa_eval_set_batch), for throughput on independent evaluation points
