@@ -90,6 +90,47 @@ def graph_us(fn, n=8 * R, reps=5):
     return e0.elapsed_time(e1) * 1e3 / (reps * n)
 
 
+def graph_us_streams(n_streams, n=8 * R, reps=5):
+    """comp() of replica r on stream r % n_streams (independent sets side by
+    side; each plan's default workspace serves one stream)"""
+    global sh
+    sts = [st] + [torch.cuda.Stream(dev) for _ in range(n_streams - 1)]
+    hs = [C.c_void_p(s.cuda_stream) for s in sts]
+
+    def fn(i):
+        global sh
+        sh = hs[(i % R) % n_streams]
+        comp(i)
+
+    for i in range(R):
+        fn(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        fork = torch.cuda.Event()
+        fork.record(st)
+        for s in sts[1:]:
+            s.wait_event(fork)
+        for i in range(n):
+            fn(i)
+        for s in sts[1:]:
+            j = torch.cuda.Event()
+            j.record(s)
+            st.wait_event(j)
+    with torch.cuda.stream(st):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        e0.record(st)
+        for _ in range(reps):
+            g.replay()
+        e1.record(st)
+    torch.cuda.synchronize()
+    sh = C.c_void_p(st.cuda_stream)
+    return e0.elapsed_time(e1) * 1e3 / (reps * n)
+
+
 if os.environ.get("EXA_NCU") == "1":
     with torch.cuda.stream(st):
         for i in range(2 * R):
@@ -100,5 +141,6 @@ out = {"workload": name, "R": R, "set_us": graph_us(set_only), "set_comp_us": gr
        "set_comp_shared_ws_us": graph_us(comp_ws),
        "set_compJ_us": graph_us(lambda i: comp(i, True, False)),
        "set_compH_us": graph_us(lambda i: comp(i, False, True)),
+       "set_comp_2streams_us": graph_us_streams(2), "set_comp_3streams_us": graph_us_streams(3),
        "nnz_jac": jp.nnz, "nnz_hess": hp.nnz, "env": {k: v for k, v in os.environ.items() if k.startswith("EXA_")}}
 print(json.dumps(out), flush=True)
