@@ -198,6 +198,16 @@ int exa_eval_cons_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, do
 int exa_eval_jac_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, double* jac_host, exa_stream_t stream);
 int exa_eval_hess_host(ExaPlan* plan, ExaWorkspace* ws, const double* x_host, const double* mult_host,
                        double obj_weight, double* hess_host, exa_stream_t stream);
+/* Page-lock a caller's pageable host range in place (cudaHostRegister,
+ * portable + mapped) so the *_host entries above use it like page-locked
+ * memory: inputs without staging, outputs written through their device
+ * mapping.  The caller unregisters it (exa_host_unregister, same ptr) before
+ * freeing it.  Non-zero status (message in exa_last_error) when the range
+ * cannot be locked -- e.g. it overlaps a registered one; it stays pageable.
+ * The Python mirror does this for numpy arrays passed again and again
+ * (a solver's scratch buffers, reference solver.py:249-295). */
+int exa_host_register(void* ptr, size_t bytes);
+int exa_host_unregister(void* ptr);
 /* ---- compressed values (what the reference solver consumes) ------------ */
 /* A compressed pattern on the plan's device (reference compress_coordinates /
  * CompressedPattern, autodiff.py:660-689): nnz compressed entries over n_raw

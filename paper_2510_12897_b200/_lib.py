@@ -76,6 +76,8 @@ SIGNATURES = {
     "exa_eval_cons_host": (C.c_int, [vp, vp, vp, vp, vp]),
     "exa_eval_jac_host": (C.c_int, [vp, vp, vp, vp, vp]),
     "exa_eval_hess_host": (C.c_int, [vp, vp, vp, vp, dbl, vp, vp]),
+    "exa_host_register": (C.c_int, [vp, C.c_size_t]),
+    "exa_host_unregister": (C.c_int, [vp]),
     "exa_eval_set_batch": (C.c_int, [vp, vp, i64, vp, vp, dbl, vp, vp, vp, vp]),
     "exa_segment_sum": (C.c_int, [i64, vp, vp, vp, vp, vp]),
     "exa_pattern_create": (C.c_int, [vp, i64, i64, vp, vp, C.POINTER(vp)]),

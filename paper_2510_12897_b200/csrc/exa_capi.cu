@@ -1559,6 +1559,29 @@ int exa_eval_hess_host(ExaPlan* p, ExaWorkspace* ws, const double* x, const doub
   return host_eval(p, ws, EXA_MODE_HESS, x, mult, w_obj, nullptr, nullptr, hess, (cudaStream_t)stream);
 }
 
+// Page-lock a caller's pageable range in place, mapped and portable, so the
+// host-buffer entries treat it like page-locked memory (H2D without staging,
+// D2H by the store kernel through its device mapping).  A failure (range
+// already registered, memory limits) leaves it pageable and clears the error.
+int exa_host_register(void* ptr, size_t bytes) {
+  if (!ptr || !bytes) return fail("exa_host_register: empty range");
+  const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail("exa_host_register: cudaHostRegister failed: %s", cudaGetErrorString(e));
+  }
+  return 0;
+}
+
+int exa_host_unregister(void* ptr) {
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail("exa_host_unregister: cudaHostUnregister failed: %s", cudaGetErrorString(e));
+  }
+  return 0;
+}
+
 static int pattern_build(ExaPlan* p, int64_t n_raw, int64_t nnz, const int64_t* ptr, const int32_t* ent,
                          const uint8_t* known, const double* known_val, ExaPattern** out,
                          const uint8_t* direct = nullptr) {
