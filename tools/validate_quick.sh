@@ -1,4 +1,4 @@
-TAG=r02v1
+TAG=${1:-r02v}
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
