@@ -135,6 +135,24 @@ class _Stage:
                 host[...] = t.cpu().numpy()
 
 
+def _dev_ptrs(dp, pairs):
+    """``data_ptr`` of every ``(tensor, length)`` when each is a contiguous 1-D
+    float64 CUDA tensor of that length on the plan's device (the per-call fast
+    path of a GPU-resident caller); else None, and the general path checks,
+    converts and raises exactly as before."""
+    dev = dp.__dict__.get("_torch_dev")
+    if dev is None:
+        return None
+    f64 = _torch().float64
+    out = []
+    for t, n in pairs:
+        if (not getattr(t, "is_cuda", False) or t.dtype != f64 or t.device != dev or t.dim() != 1
+                or t.shape[0] != n or not t.is_contiguous()):
+            return None
+        out.append(t.data_ptr())
+    return out
+
+
 def _check_x(model, x):
     if _is_cuda(x):
         if tuple(x.shape) != (model.nvar,):
@@ -405,9 +423,19 @@ def eval_callback_set(model, x, mult, obj_weight: float, out_c, out_jac, out_hes
     Equivalent to ``eval_constraints`` + ``eval_jacobian`` + ``eval_hessian``;
     a domain error is reported as the first of those three would report it.
     """
+    plan = model.plan
+    dp = model.device_plan
+    if dp is not None and getattr(x, "is_cuda", False):
+        p = _dev_ptrs(dp, ((x, model.nvar), (mult, model.ncon), (out_c, model.ncon), (out_jac, plan.n_jac_slots),
+                           (out_hess, plan.n_hess_slots)))
+        if p is not None:  # all device tensors, nothing to convert or stage
+            s = C.c_void_p(_torch()._C._cuda_getCurrentRawStream(dp.device))
+            _lib.check(dp._lib.exa_eval_set(dp.handle, dp.workspace(), p[0], p[1] if model.ncon else 0,
+                                            float(obj_weight), p[2], p[3], p[4], s), "eval_set")
+            _raise_domain(dp, s, "set")
+            return
     x = _check_x(model, x)
     mult = _check_mult(model, mult)
-    plan = model.plan
     for buf, n, what in ((out_c, model.ncon, "constraint"), (out_jac, plan.n_jac_slots, "jacobian"),
                          (out_hess, plan.n_hess_slots, "hessian")):
         if _shape(buf) != (n,):
