@@ -231,7 +231,8 @@ class _HostPins:
     numpy API: 1.97k -> ~3.0k sets/s, the page-locked figure).
 
     An array is locked on its SECOND use (a one-shot array never pays the lock)
-    when it owns its memory and holds at least ``MIN_BYTES``; the lock is
+    when it owns its memory (or is a view holding at least about half of its
+    owner) and holds at least ``MIN_BYTES``; the lock is
     dropped by a weakref finalizer, which numpy runs before it frees the
     memory.  Arrays may share a page (heap neighbours: the driver accepts
     registrations that share pages, not ones that share bytes); a range the
@@ -240,6 +241,7 @@ class _HostPins:
 
     MIN_BYTES = 1 << 18
     MAX_BYTES = 8 << 30
+    SLACK_BYTES = 64 << 20  # an owner may exceed twice the passed view by this much
 
     def __init__(self):
         import os
@@ -265,8 +267,8 @@ class _HostPins:
         if not self.enabled or a.nbytes < self.MIN_BYTES:
             return
         o = self._owner(a)
-        if o is None:
-            return
+        if o is None or o.nbytes > 2 * a.nbytes + self.SLACK_BYTES:
+            return  # a small view of a much larger owner does not lock all of it
         key = id(o)
         with self._mu:
             if key in self._spans:  # (numpy refuses ndarray.resize of a weak-referenced array)

@@ -71,6 +71,20 @@ def test_views_lock_their_owner_once():
     assert not lib.live
 
 
+def test_small_view_of_a_large_owner_is_skipped():
+    pins, lib = _pins(), FakeLib()
+    pins.SLACK_BYTES = 0
+    owner = np.empty(8 * pins.MIN_BYTES // 8)
+    small = owner[:pins.MIN_BYTES // 8]
+    for _ in range(3):
+        pins.note(lib, small)
+    assert not lib.calls
+    big = owner[pins.MIN_BYTES // 8:]
+    pins.note(lib, big)
+    pins.note(lib, big)
+    assert lib.live == {owner.ctypes.data: owner.nbytes} and pins.locked(small)
+
+
 def test_arrays_not_owning_memory_are_skipped():
     pins, lib = _pins(), FakeLib()
     buf = bytearray(pins.MIN_BYTES)
