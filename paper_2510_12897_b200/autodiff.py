@@ -621,6 +621,19 @@ def eval_callback_set_compressed(model, x, mult, obj_weight: float, out_c, out_j
     bit-identical to ``pattern.sum_values(raw)``.  One set kernel writes the raw
     slots into device scratch and one segmented-sum launch compresses them; for
     numpy buffers only c and the compressed values cross PCIe."""
+    dp = model.device_plan
+    hd = dp.__dict__.get("_cmp_handles") if dp is not None else None
+    if hd is not None and getattr(x, "is_cuda", False):
+        jp, hp, jh, hh = hd
+        p = _dev_ptrs(dp, ((x, model.nvar), (mult, model.ncon), (out_c, model.ncon), (out_jac, jp.nnz),
+                           (out_hess, hp.nnz)))
+        if p is not None:  # all device tensors, patterns already on this plan's device
+            s = C.c_void_p(_torch()._C._cuda_getCurrentRawStream(dp.device))
+            _lib.check(dp._lib.exa_eval_set_compressed(dp.handle, dp.workspace(), jh, hh, p[0],
+                                                       p[1] if model.ncon else 0, float(obj_weight), p[2], p[3],
+                                                       p[4], s), "eval_set_compressed")
+            _raise_domain(dp, s, "set")
+            return
     x = _check_x(model, x)
     mult = _check_mult(model, mult)
     jp, hp = model_patterns(model)
@@ -630,6 +643,7 @@ def eval_callback_set_compressed(model, x, mult, obj_weight: float, out_c, out_j
             raise ValueError(f"{what} buffer has shape {_shape(buf)}, expected ({n},)")
     dp = _dplan(model)
     jh, hh = jp.device_handle(dp, "jac"), hp.device_handle(dp, "hess")
+    dp._cmp_handles = (jp, hp, jh, hh)
     if not _is_cuda(x) and not _is_cuda(mult) and _host_outputs(out_c, out_jac, out_hess):
         return _host_call(dp, "exa_eval_set_compressed_host", "set", jh, hh, x, mult, float(obj_weight),
                           out_c, out_jac, out_hess)
